@@ -1,0 +1,137 @@
+/*
+ * tenvec_b200.h -- C-ABI of libtenvec_b200.so, the B200 (sm_100a) hot path of
+ * arXiv 2501.03121 (native TVC, dTVC reductions, dHOPM3 normalisation).
+ *
+ * Every entry point takes plain device pointers owned by the caller, element
+ * counts, and a cudaStream_t passed as void*.  All work is enqueued
+ * asynchronously on that stream; nothing here allocates device memory or
+ * synchronises the host.  Return value: TV_OK (0) or an error code; the
+ * thread-local tv_last_error() gives the message.  There is no CPU fallback:
+ * a missing or failing device raises TV_ECUDA.
+ *
+ * Reference interfaces replaced (paths relative to the reference pkg/src/tenvec):
+ *   tv_tvc          kernels.py:126-171  tvc_native (and getvc, kernels.py:73-123,
+ *                                       through the (u, n_k, v) block view)
+ *   tv_getvc        kernels.py:73-123   getvc over a strided m x n view (lda >= n)
+ *   tv_convert      precision.py:109-128 promote / demote (bit-exact semantics)
+ *   tv_norm2        kernels.py:234-239  norm2
+ *   tv_normalize    kernels.py:242-254  normalize
+ *   tv_rank_fold    comm.py:84-100      ring_all_reduce (ascending-rank fold) and
+ *                   comm.py:103-134     ring_all_reduce_mixed (chunk c starts at rank c,
+ *                                       demote(promote+promote) per hop)
+ *   tv_fill         bench.py:62-80      fill_array (ones / ramp; "hash" replaces numpy's
+ *                                       integer-random with a counter hash in [1, 97])
+ */
+#ifndef TENVEC_B200_H
+#define TENVEC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* storage / compute element types (precision.py:69-87) */
+typedef enum {
+  TV_F64 = 0,  /* double                                   */
+  TV_F32 = 1,  /* single                                   */
+  TV_F16 = 2,  /* IEEE binary16 ("half")                   */
+  TV_BF16 = 3  /* brain float, uint16 bit pattern ("brain") */
+} tv_dtype;
+
+/* error codes; Python maps 1->KernelError, 2->ModeError, 3->NormalizationError,
+ * 4->CollectiveError, 5->CUDA runtime error */
+enum {
+  TV_OK = 0,
+  TV_EKERNEL = 1,
+  TV_EMODE = 2,
+  TV_ENORM = 3,
+  TV_ECOLL = 4,
+  TV_ECUDA = 5
+};
+
+/* fill kinds for tv_fill */
+enum { TV_FILL_ONES = 0, TV_FILL_RAMP = 1, TV_FILL_HASH = 2 };
+
+/* maximum rank count of tv_rank_fold */
+#define TV_MAX_RANKS 64
+
+/* Library version string and the kernel regime names (diagnostics). */
+const char* tv_version(void);
+const char* tv_last_error(void);
+
+/* Y = alpha * (A x_k x) + beta * Y over the rank-local block view
+ * A[u][nk][v] (last index fastest, no unfolding copy).  Valid (storage,
+ * compute) pairs: (F64,F64) (F32,F32) (F32,F64) (F16,F32) (BF16,F32).
+ * beta == 0 never reads y.  y holds u*v storage elements.  Accumulation in
+ * the compute type, one demote on store; alpha multiplies the finished dot
+ * product and beta*y is added after it (kernels.py:113-119).  The reduction
+ * order per output element is fixed by (u, nk, v, dtype): reruns and ranks
+ * reproduce bits. */
+int tv_tvc(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
+           const void* x, double alpha, double beta, void* y, void* stream);
+
+/* The same contraction through the naive scalar kernel only (one thread per
+ * output for v > 1, one warp per row for v == 1): the "looped" cross-check of
+ * tv_tvc's regime kernels, used by tvc_looped_oracle (kernels.py:174-188). */
+int tv_tvc_naive(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
+                 const void* x, double alpha, double beta, void* y, void* stream);
+
+/* Which kernel regime tv_tvc would pick for this view (0 generic, 1 rows,
+ * 2 short rows, 3 columns, 4 narrow slabs); -1 on invalid arguments. */
+int tv_tvc_regime(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
+
+/* getvc over an m x n row-major view with leading dimension lda >= n.
+ * trans 0 = matvec (x has n, y has m), 1 = vecmat (x has m, y has n). */
+int tv_getvc(int trans, const void* A, int storage, int compute, int64_t m, int64_t n,
+             int64_t lda, const void* x, double alpha, double beta, void* y, void* stream);
+
+/* dst[i] = convert(src[i]) with reference semantics: widening is exact,
+ * f64->f32 and ->f16 round to nearest even (f16 overflow -> inf), ->bf16
+ * rounds to f32 first and truncates the low 16 bits. */
+int tv_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n,
+               void* stream);
+
+/* *norm_out (device double) = sqrt(sum promote(x)^2) accumulated in the
+ * compute type with a fixed reduction tree (single CTA). */
+int tv_norm2(const void* x, int storage, int compute, int64_t n, double* norm_out,
+             void* stream);
+
+/* x <- demote(promote(x) / ||x||) in place; *norm_out (device double) gets
+ * the norm it had.  A zero norm leaves x untouched and sets *status_out
+ * (device int32) to TV_ENORM; status_out may be NULL. */
+int tv_normalize(void* x, int storage, int compute, int64_t n, double* norm_out,
+                 int32_t* status_out, void* stream);
+
+/* Rank-ordered fold of p device buffers (srcs is a HOST array of p device
+ * pointers, p <= TV_MAX_RANKS) into dst (may alias srcs[0]).
+ *   mixed == 0: dst[e] = ((s0[e] + s1[e]) + s2[e]) + ...  in the storage type
+ *               (exact-width ring_all_reduce, bit-equal to serial_rank_sum)
+ *   mixed != 0: with c = chunk ? e / chunk : 0 and r0 = (start + c) % p,
+ *               cur = s_r0[e]; for i in 1..p-1: cur = demote(promote(cur) +
+ *               promote(s_{(r0+i)%p}[e]))  (ring_all_reduce_mixed)
+ * chunk is ring_chunks' ceil(n/p) for an in-process fold over whole
+ * buffers, or 0 with start = c when the buffers hold only chunk c. */
+int tv_rank_fold(const void* const* srcs, int p, int64_t n, int64_t chunk, int start,
+                 int storage, int compute, int mixed, void* dst, void* stream);
+
+/* Same fold, sources at src + r * src_stride_elems (one contiguous receive
+ * buffer after an all-to-all). */
+int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64_t n,
+                         int64_t chunk, int start, int storage, int compute, int mixed,
+                         void* dst, void* stream);
+
+/* Fill the rank-local slab [s_lo, s_hi) along mode s of a global tensor with
+ * extents ext[0..d-1] (last mode fastest) from the GLOBAL linear index g:
+ * ones -> 1, ramp -> (g mod 97) + 1, hash -> (splitmix64(seed, g) mod 97) + 1. */
+int tv_fill(void* A, int dtype, int kind, uint64_t seed, const int64_t* ext, int d, int s,
+            int64_t s_lo, int64_t s_hi, void* stream);
+
+/* Number of SMs of the current device (grid sizing diagnostics). */
+int tv_device_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TENVEC_B200_H */

@@ -1,0 +1,93 @@
+"""ctypes binding of libtenvec_b200.so (include/tenvec_b200.h).
+
+The library is the only compute path of this package: there is no CPU
+fallback.  Loading fails loudly when the .so is missing, and every device
+entry point checks that CUDA is available before it is called.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from .errors import CollectiveError, DeviceError, KernelError, ModeError, NormalizationError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libtenvec_b200.so"
+
+# tv_dtype codes
+TV_F64, TV_F32, TV_F16, TV_BF16 = 0, 1, 2, 3
+TV_FILL_ONES, TV_FILL_RAMP, TV_FILL_HASH = 0, 1, 2
+TV_MAX_RANKS = 64
+REGIMES = {0: "generic", 1: "rows", 2: "rows_short", 3: "cols", 4: "slabs"}
+
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_int = ctypes.c_int
+
+# symbol -> (restype, argtypes); the list every test checks is exported
+SIGNATURES = {
+    "tv_version": (ctypes.c_char_p, []),
+    "tv_last_error": (ctypes.c_char_p, []),
+    "tv_tvc": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),
+    "tv_tvc_naive": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),
+    "tv_tvc_regime": (_int, [_vp, _int, _i64, _i64, _i64]),
+    "tv_getvc": (_int, [_int, _vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),
+    "tv_convert": (_int, [_vp, _int, _vp, _int, _i64, _vp]),
+    "tv_norm2": (_int, [_vp, _int, _int, _i64, _vp, _vp]),
+    "tv_normalize": (_int, [_vp, _int, _int, _i64, _vp, _vp, _vp]),
+    "tv_rank_fold": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _int, _int, _int, _vp, _vp]),
+    "tv_rank_fold_strided": (_int, [_vp, _i64, _int, _i64, _i64, _int, _int, _int, _int, _vp, _vp]),
+    "tv_fill": (_int, [_vp, _int, _int, ctypes.c_uint64, ctypes.POINTER(_i64), _int, _int, _i64, _i64, _vp]),
+    "tv_device_sms": (_int, []),
+}
+
+_ERRORS = {1: KernelError, 2: ModeError, 3: NormalizationError, 4: CollectiveError, 5: DeviceError}
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def load(path: Path | str | None = None) -> ctypes.CDLL:
+    """Load (once) and return the library; raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"{p} is missing: build it with `python -m paper_2501_03121_b200.build` "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    lib = load()
+    msg = lib.tv_last_error().decode(errors="replace")
+    exc = _ERRORS.get(rc, DeviceError)
+    raise exc(f"{what}: {msg}" if what else msg)
+
+
+def require_cuda() -> None:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("a CUDA device is required: libtenvec_b200 has no CPU path")
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

@@ -1,0 +1,43 @@
+// Host-side helpers shared by the translation units of libtenvec_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tenvec_b200.h"
+
+namespace tv {
+
+// kernel regimes of tv_tvc (reported by tv_tvc_regime)
+enum { REG_GENERIC = 0, REG_ROWS = 1, REG_ROWS_SHORT = 2, REG_COLS = 3, REG_SLABS = 4 };
+
+// the five valid (storage, compute) pairs of precision.py:81-87
+enum { MODE_INVALID = -1, MODE_F64 = 0, MODE_F32 = 1, MODE_F32F64 = 2, MODE_F16F32 = 3, MODE_BF16F32 = 4 };
+
+inline int mode_id(int storage, int compute) {
+  if (storage == TV_F64 && compute == TV_F64) return MODE_F64;
+  if (storage == TV_F32 && compute == TV_F32) return MODE_F32;
+  if (storage == TV_F32 && compute == TV_F64) return MODE_F32F64;
+  if (storage == TV_F16 && compute == TV_F32) return MODE_F16F32;
+  if (storage == TV_BF16 && compute == TV_F32) return MODE_BF16F32;
+  return MODE_INVALID;
+}
+
+inline int dtype_bytes(int dt) {
+  switch (dt) {
+    case TV_F64: return 8;
+    case TV_F32: return 4;
+    case TV_F16:
+    case TV_BF16: return 2;
+    default: return -1;
+  }
+}
+
+int set_error(int code, const char* msg);
+int check_launch(const char* what);
+int regime_of(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
+int tvc_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
+                 int64_t su, int64_t sk, const void* x, double alpha, double beta, void* y,
+                 void* stream, int force_generic);
+
+}  // namespace tv

@@ -1,0 +1,324 @@
+// Conversions, normalisation, rank-ordered folds and on-device fills.
+//
+//   tv_convert      precision.py:109-128 (promote / demote, bit-exact)
+//   tv_norm2        kernels.py:234-239   (norm2 in the compute type)
+//   tv_normalize    kernels.py:242-254   (x <- demote(promote(x) / ||x||))
+//   tv_rank_fold    comm.py:84-100       (exact ring allreduce = ascending-rank sum)
+//                   comm.py:103-134      (mixed ring: chunk c starts at rank c,
+//                                         demote(promote + promote) per hop)
+//   tv_fill         bench.py:62-80       (ones / ramp over the GLOBAL index; the
+//                                         counter hash stands in for numpy's rng)
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tv_internal.h"
+#include "tv_types.cuh"
+
+namespace tv {
+
+static thread_local std::string g_err;
+
+int set_error(int code, const char* msg) {
+  g_err = msg ? msg : "";
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    return set_error(TV_ECUDA, m.c_str());
+  }
+  return TV_OK;
+}
+
+// ------------------------------------------------------------- convert ----
+template <int SRC>
+struct Wide {
+  using W = float;
+};
+template <>
+struct Wide<TV_F64> {
+  using W = double;
+};
+
+template <int SRC>
+__device__ __forceinline__ typename Wide<SRC>::W widen(typename St<SRC>::T v) {
+  if constexpr (SRC == TV_F64) return v;
+  else if constexpr (SRC == TV_F32) return v;
+  else if constexpr (SRC == TV_F16) return __half2float(__ushort_as_half(v));
+  else return __uint_as_float(((uint32_t)v) << 16);
+}
+
+template <int DST, typename W>
+__device__ __forceinline__ typename St<DST>::T narrow(W w) {
+  if constexpr (DST == TV_F64) {
+    return (double)w;
+  } else if constexpr (DST == TV_F32) {
+    if constexpr (sizeof(W) == 8) return __double2float_rn(w);
+    else return w;
+  } else if constexpr (DST == TV_F16) {
+    // one RNE rounding straight from the source width (numpy astype)
+    if constexpr (sizeof(W) == 8) return __half_as_ushort(__double2half(w));
+    else return __half_as_ushort(__float2half_rn(w));
+  } else {
+    // brain: RNE to binary32 first, then truncate (precision.py:125-126)
+    float f;
+    if constexpr (sizeof(W) == 8) f = __double2float_rn(w);
+    else f = w;
+    return (uint16_t)(__float_as_uint(f) >> 16);
+  }
+}
+
+template <int SRC, int DST>
+__global__ void k_convert(const typename St<SRC>::T* __restrict__ src,
+                          typename St<DST>::T* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = narrow<DST>(widen<SRC>(src[i]));
+}
+
+static unsigned grid_1d(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > 148LL * 64) b = 148LL * 64;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+template <int SRC>
+static int convert_from(const void* src, int dst_dt, void* dst, int64_t n, cudaStream_t st) {
+  const unsigned g = grid_1d(n, 256);
+  using S = typename St<SRC>::T;
+  switch (dst_dt) {
+    case TV_F64: k_convert<SRC, TV_F64><<<g, 256, 0, st>>>((const S*)src, (double*)dst, n); break;
+    case TV_F32: k_convert<SRC, TV_F32><<<g, 256, 0, st>>>((const S*)src, (float*)dst, n); break;
+    case TV_F16: k_convert<SRC, TV_F16><<<g, 256, 0, st>>>((const S*)src, (uint16_t*)dst, n); break;
+    case TV_BF16: k_convert<SRC, TV_BF16><<<g, 256, 0, st>>>((const S*)src, (uint16_t*)dst, n); break;
+    default: return set_error(TV_EMODE, "tv_convert: bad destination dtype");
+  }
+  return check_launch("tv_convert");
+}
+
+// ---------------------------------------------------------------- norm ----
+// one CTA of 1024 threads: strided per-thread sums, xor-shuffle per warp, then
+// warp 0 folds the 32 warp sums -- a fixed tree, so every rank that holds the
+// same vector computes the same bits (hopm.py:339-342 checks exactly that).
+template <int SD, typename C>
+__global__ void __launch_bounds__(1024)
+    k_norm(typename St<SD>::T* __restrict__ x, int64_t n, double* __restrict__ norm_out,
+           int32_t* __restrict__ status, int do_scale) {
+  __shared__ C part[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  C s = C(0);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const C c = promote<SD, C>(x[i]);
+    s = fma(c, c, s);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) part[w] = s;
+  __syncthreads();
+  if (w == 0) {
+    s = lane < (int)(blockDim.x >> 5) ? part[lane] : C(0);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) part[0] = s;
+  }
+  __syncthreads();
+  const C nrm = sqrt(part[0]);
+  if (threadIdx.x == 0) {
+    norm_out[0] = (double)nrm;
+    if (status) status[0] = (nrm == C(0)) ? TV_ENORM : TV_OK;
+  }
+  if (do_scale && nrm != C(0)) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      x[i] = demote<SD, C>(promote<SD, C>(x[i]) / nrm);
+  }
+}
+
+static int norm_dispatch(void* x, int storage, int compute, int64_t n, double* norm_out,
+                         int32_t* status, int do_scale, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (n < 0 || norm_out == nullptr || (n > 0 && x == nullptr))
+    return set_error(TV_EKERNEL, "tv_norm: bad arguments");
+  switch (mode_id(storage, compute)) {
+    case MODE_F64: k_norm<TV_F64, double><<<1, 1024, 0, st>>>((double*)x, n, norm_out, status, do_scale); break;
+    case MODE_F32: k_norm<TV_F32, float><<<1, 1024, 0, st>>>((float*)x, n, norm_out, status, do_scale); break;
+    case MODE_F32F64: k_norm<TV_F32, double><<<1, 1024, 0, st>>>((float*)x, n, norm_out, status, do_scale); break;
+    case MODE_F16F32: k_norm<TV_F16, float><<<1, 1024, 0, st>>>((uint16_t*)x, n, norm_out, status, do_scale); break;
+    case MODE_BF16F32: k_norm<TV_BF16, float><<<1, 1024, 0, st>>>((uint16_t*)x, n, norm_out, status, do_scale); break;
+    default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
+  }
+  return check_launch("tv_norm");
+}
+
+// ---------------------------------------------------------------- fold ----
+struct Srcs {
+  const void* p[TV_MAX_RANKS];
+};
+
+template <int SD, typename C>
+__global__ void k_fold(Srcs srcs, int p, int64_t n, int64_t chunk, int start, int mixed,
+                       typename St<SD>::T* __restrict__ dst) {
+  using T = typename St<SD>::T;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    T cur;
+    if (!mixed) {
+      // ascending-rank fold in the storage format (comm.py:95-97)
+      cur = reinterpret_cast<const T*>(srcs.p[0])[e];
+      for (int r = 1; r < p; ++r) {
+        const T b = reinterpret_cast<const T*>(srcs.p[r])[e];
+        if constexpr (SD == TV_F64 || SD == TV_F32) cur = add_rn(cur, b);
+        else cur = demote<SD, C>(add_rn(promote<SD, C>(cur), promote<SD, C>(b)));
+      }
+    } else {
+      // chunk c starts at rank c, each hop demote(promote + promote) (comm.py:123-130)
+      const int64_t c = chunk > 0 ? e / chunk : 0;
+      const int r0 = (int)((start + c) % p);
+      cur = reinterpret_cast<const T*>(srcs.p[r0])[e];
+      for (int i = 1; i < p; ++i) {
+        const int r = (r0 + i) % p;
+        const T b = reinterpret_cast<const T*>(srcs.p[r])[e];
+        cur = demote<SD, C>(add_rn(promote<SD, C>(cur), promote<SD, C>(b)));
+      }
+    }
+    dst[e] = cur;
+  }
+}
+
+static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int start, int storage,
+                         int compute, int mixed, void* dst, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p < 1 || p > TV_MAX_RANKS || n < 0 || start < 0 || chunk < 0)
+    return set_error(TV_ECOLL, "tv_rank_fold: bad rank count / length / chunk");
+  if (n == 0) return TV_OK;
+  const unsigned g = grid_1d(n, 256);
+  switch (mode_id(storage, compute)) {
+    case MODE_F64: k_fold<TV_F64, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (double*)dst); break;
+    case MODE_F32: k_fold<TV_F32, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (float*)dst); break;
+    case MODE_F32F64: k_fold<TV_F32, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (float*)dst); break;
+    case MODE_F16F32: k_fold<TV_F16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (uint16_t*)dst); break;
+    case MODE_BF16F32: k_fold<TV_BF16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (uint16_t*)dst); break;
+    default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
+  }
+  return check_launch("tv_rank_fold");
+}
+
+// ---------------------------------------------------------------- fill ----
+__host__ __device__ inline uint64_t fill_hash(uint64_t seed, uint64_t g) {
+  uint64_t z = (g + 1ULL) * 0x9E3779B97F4A7C15ULL + seed * 0xD1B54A32D192ED03ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+template <int SD>
+__global__ void k_fill(typename St<SD>::T* __restrict__ A, int64_t total, int kind, uint64_t seed,
+                       int64_t V, int64_t q, int64_t ns, int64_t lo) {
+  const int64_t qV = q * V;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pre = e / qV;
+    const int64_t rem = e - pre * qV;
+    const int64_t is = rem / V;
+    const int64_t suf = rem - is * V;
+    const uint64_t g = (uint64_t)((pre * ns + lo + is) * V + suf);
+    float val;
+    if (kind == TV_FILL_ONES) val = 1.0f;
+    else if (kind == TV_FILL_RAMP) val = (float)(g % 97ULL) + 1.0f;
+    else val = (float)(fill_hash(seed, g) % 97ULL) + 1.0f;
+    A[e] = narrow<SD>(val);  // integers <= 97 are exact in every storage format
+  }
+}
+
+}  // namespace tv
+
+// ================================================================ C-ABI ====
+extern "C" const char* tv_version(void) { return "tenvec_b200 0.1.0 (sm_100a)"; }
+extern "C" const char* tv_last_error(void) { return tv::g_err.c_str(); }
+
+extern "C" int tv_device_sms(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return n;
+}
+
+extern "C" int tv_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n,
+                          void* stream) {
+  using namespace tv;
+  if (n < 0) return set_error(TV_EKERNEL, "tv_convert: negative length");
+  if (n == 0) return TV_OK;
+  if (!src || !dst) return set_error(TV_EKERNEL, "tv_convert: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (src_dtype) {
+    case TV_F64: return convert_from<TV_F64>(src, dst_dtype, dst, n, st);
+    case TV_F32: return convert_from<TV_F32>(src, dst_dtype, dst, n, st);
+    case TV_F16: return convert_from<TV_F16>(src, dst_dtype, dst, n, st);
+    case TV_BF16: return convert_from<TV_BF16>(src, dst_dtype, dst, n, st);
+    default: return set_error(TV_EMODE, "tv_convert: bad source dtype");
+  }
+}
+
+extern "C" int tv_norm2(const void* x, int storage, int compute, int64_t n, double* norm_out,
+                        void* stream) {
+  return tv::norm_dispatch(const_cast<void*>(x), storage, compute, n, norm_out, nullptr, 0, stream);
+}
+
+extern "C" int tv_normalize(void* x, int storage, int compute, int64_t n, double* norm_out,
+                            int32_t* status_out, void* stream) {
+  return tv::norm_dispatch(x, storage, compute, n, norm_out, status_out, 1, stream);
+}
+
+extern "C" int tv_rank_fold(const void* const* srcs, int p, int64_t n, int64_t chunk, int start,
+                            int storage, int compute, int mixed, void* dst, void* stream) {
+  using namespace tv;
+  if (!srcs || p < 1 || p > TV_MAX_RANKS) return set_error(TV_ECOLL, "tv_rank_fold: bad sources");
+  Srcs s{};
+  for (int r = 0; r < p; ++r) {
+    if (!srcs[r] && n > 0) return set_error(TV_ECOLL, "tv_rank_fold: null source");
+    s.p[r] = srcs[r];
+  }
+  return fold_dispatch(s, p, n, chunk, start, storage, compute, mixed, dst, stream);
+}
+
+extern "C" int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64_t n,
+                                    int64_t chunk, int start, int storage, int compute, int mixed,
+                                    void* dst, void* stream) {
+  using namespace tv;
+  if (!src || p < 1 || p > TV_MAX_RANKS || src_stride_elems < n)
+    return set_error(TV_ECOLL, "tv_rank_fold_strided: bad arguments");
+  const int sb = dtype_bytes(storage);
+  if (sb <= 0) return set_error(TV_EMODE, "tv_rank_fold_strided: bad storage dtype");
+  Srcs s{};
+  for (int r = 0; r < p; ++r)
+    s.p[r] = static_cast<const char*>(src) + (size_t)r * (size_t)src_stride_elems * (size_t)sb;
+  return fold_dispatch(s, p, n, chunk, start, storage, compute, mixed, dst, stream);
+}
+
+extern "C" int tv_fill(void* A, int dtype, int kind, uint64_t seed, const int64_t* ext, int d,
+                       int s, int64_t s_lo, int64_t s_hi, void* stream) {
+  using namespace tv;
+  if (!ext || d < 1 || s < 0 || s >= d || s_lo < 0 || s_hi <= s_lo || s_hi > ext[s])
+    return set_error(TV_EKERNEL, "tv_fill: bad extents / slab range");
+  if (kind < TV_FILL_ONES || kind > TV_FILL_HASH) return set_error(TV_EKERNEL, "tv_fill: bad kind");
+  int64_t V = 1, pre = 1;
+  for (int i = s + 1; i < d; ++i) V *= ext[i];
+  for (int i = 0; i < s; ++i) pre *= ext[i];
+  const int64_t q = s_hi - s_lo;
+  const int64_t total = pre * q * V;
+  if (total == 0) return TV_OK;
+  if (!A) return set_error(TV_EKERNEL, "tv_fill: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned g = grid_1d(total, 256);
+  switch (dtype) {
+    case TV_F64: k_fill<TV_F64><<<g, 256, 0, st>>>((double*)A, total, kind, seed, V, q, ext[s], s_lo); break;
+    case TV_F32: k_fill<TV_F32><<<g, 256, 0, st>>>((float*)A, total, kind, seed, V, q, ext[s], s_lo); break;
+    case TV_F16: k_fill<TV_F16><<<g, 256, 0, st>>>((uint16_t*)A, total, kind, seed, V, q, ext[s], s_lo); break;
+    case TV_BF16: k_fill<TV_BF16><<<g, 256, 0, st>>>((uint16_t*)A, total, kind, seed, V, q, ext[s], s_lo); break;
+    default: return set_error(TV_EMODE, "tv_fill: bad dtype");
+  }
+  return check_launch("tv_fill");
+}

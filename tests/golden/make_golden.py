@@ -1,0 +1,187 @@
+"""Generate tests/golden/*.npz by running the REFERENCE package itself.
+
+Run here (the container that has /root/reference); the GPU box only reads the
+committed .npz files:
+
+    python tests/golden/make_golden.py [--ref /root/reference/pkg/src]
+
+Every fixture is the reference's own output on seeded inputs: the oracle
+(oracle/tenvec_oracle.py) is pinned against these, and the GPU parity tests
+compare the CUDA path against both.  Cases follow the reference tests:
+test_kernels.py:77-89 (200 random integer shapes), test_acceptance.py:28-76
+(SHAPE_SUITE dtvc over every k, s, p), test_acceptance.py:189-218 and
+test_comm.py (precision and ring folds), test_hopm.py / test_acceptance.py:79-96
+(power method).
+"""
+
+from __future__ import annotations
+
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+
+SHAPE_SUITE = [(2, 2), (3, 5), (6, 6), (2, 3, 4), (4, 4, 4), (5, 2, 6), (2, 3, 2, 4),
+               (3, 3, 3, 3), (2, 2, 3, 2, 4)]
+MODE_SHAPES = [(7,), (3, 5), (5, 8), (4, 6, 5), (2, 3, 4, 5), (6, 1, 9), (3, 40, 8), (2, 9, 33)]
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref", default="/root/reference/pkg/src")
+    args = ap.parse_args()
+    sys.path.insert(0, args.ref)
+    import tenvec as T  # the reference package
+
+    # -- precision ---------------------------------------------------------
+    spots = np.array([1.0, np.pi, 2.0, -1.5, 1e-38, 1.1754944e-38, 65504.0, 3.0e38, -7.25e-5,
+                      1.0 + 2.0 ** -9, 1.0 + 2.0 ** -8 + 2.0 ** -20])
+    rng = np.random.default_rng(17)
+    hvals = np.concatenate([
+        rng.uniform(-70000, 70000, 600), rng.uniform(-1e-4, 1e-4, 300),
+        rng.uniform(-6e-8, 6e-8, 100),
+        np.array([65504.0, 65519.9, 65520.0, 2.0 ** -25, -(2.0 ** -25), 0.0, 2.0 ** -24 * 1.5]),
+    ])
+    prec = {
+        "spots": spots,
+        "spots_bf16": T.demote(spots, T.BF16F32),
+        "spots_f32": T.demote(spots, T.F32),
+        "hvals": hvals,
+        "hvals_f16": T.demote(hvals, T.F16F32),
+        "hvals_f16_from_f32": T.demote(hvals.astype(np.float32), T.F16F32),
+        "hvals_bf16": T.demote(hvals, T.BF16F32),
+        "bf16_widen": T.promote(T.demote(spots, T.BF16F32), T.BF16F32),
+    }
+    np.savez_compressed(HERE / "precision.npz", **prec)
+
+    # -- tvc on 200 random integer shapes (test_kernels.py:77-89) ------------
+    rng = np.random.default_rng(1234)
+    out = {}
+    for i in range(200):
+        d = int(rng.integers(2, 6))
+        extents = tuple(int(e) for e in rng.integers(1, 7, d))
+        vals = rng.integers(1, 97, extents).astype(float)
+        t = T.Tensor.from_array(vals)
+        k = int(rng.integers(0, d))
+        x = rng.integers(1, 97, extents[k]).astype(float)
+        y = T.tvc_native(t, x, k)
+        out[f"c{i}_shape"] = np.array(extents)
+        out[f"c{i}_k"] = np.array(k)
+        out[f"c{i}_vals"] = vals.reshape(-1)
+        out[f"c{i}_x"] = x
+        out[f"c{i}_y"] = y.to_float64().reshape(-1)
+    out["n"] = np.array(200)
+    np.savez_compressed(HERE / "tvc_int.npz", **out)
+
+    # -- tvc in every precision mode, float data, alpha/beta ---------------
+    rng = np.random.default_rng(77)
+    out = {}
+    c = 0
+    for name in sorted(T.MODES):
+        mode = T.MODES[name]
+        for shape in MODE_SHAPES:
+            for k in range(len(shape)):
+                vals = rng.standard_normal(shape)
+                t = T.Tensor.from_array(vals, mode)
+                x = T.demote(rng.standard_normal(shape[k]), mode).copy()
+                alpha, beta = (1.0, 0.0) if c % 3 else (1.5, -0.75)
+                y0 = T.demote(rng.standard_normal(t.size // shape[k]), mode).copy()
+                y = T.tvc_native(t, x, k, alpha=alpha, beta=beta, out=y0.copy())
+                out[f"c{c}_mode"] = np.array(name)
+                out[f"c{c}_shape"] = np.array(shape)
+                out[f"c{c}_k"] = np.array(k)
+                out[f"c{c}_buf"] = t.buf
+                out[f"c{c}_x"] = x
+                out[f"c{c}_y0"] = y0
+                out[f"c{c}_ab"] = np.array([alpha, beta])
+                out[f"c{c}_y"] = y.buf.copy()
+                c += 1
+    out["n"] = np.array(c)
+    np.savez_compressed(HERE / "tvc_modes.npz", **out)
+
+    # -- ring folds (comm.py:84-134) ----------------------------------------
+    rng = np.random.default_rng(31)
+    out = {}
+    c = 0
+    for name in ("f64", "f32", "f32f64", "f16f32", "bf16f32"):
+        mode = T.MODES[name]
+        for p in (2, 3, 4, 5, 8):
+            for n in (1, 4, 10, 11, 24, 37):
+                ranks = [T.demote(rng.uniform(-4, 4, n), mode).copy() for _ in range(p)]
+                bufs = [r.copy() for r in ranks]
+                if mode.mixed:
+                    T.ring_all_reduce_mixed(bufs, mode)
+                else:
+                    T.ring_all_reduce(bufs)
+                out[f"c{c}_mode"] = np.array(name)
+                out[f"c{c}_ranks"] = np.stack(ranks)
+                out[f"c{c}_out"] = bufs[0]
+                c += 1
+    out["n"] = np.array(c)
+    np.savez_compressed(HERE / "ring.npz", **out)
+
+    # -- dtvc over SHAPE_SUITE (test_acceptance.py:54-76) -------------------
+    out = {}
+    c = 0
+    for shape in SHAPE_SUITE:
+        rng = np.random.default_rng(len(shape))
+        vals = rng.integers(-4, 5, shape).astype(float)
+        t = T.Tensor.from_array(vals)
+        d = len(shape)
+        for k in range(d):
+            x = np.random.default_rng(10 * k + 1).integers(-4, 5, shape[k]).astype(float)
+            for s in range(d):
+                for p in sorted({1, 2, 3, shape[s]}):
+                    for defer in ((False, True) if k == s else (False,)):
+                        res = T.dtvc(T.distribute(t, s, p), x, k, defer=defer)
+                        got = T.undistribute(res).to_float64().reshape(-1)
+                        out[f"c{c}"] = np.concatenate([[len(shape)], shape, [k, s, p, int(defer)], got])
+                        c += 1
+        out[f"vals{SHAPE_SUITE.index(shape)}"] = vals.reshape(-1)
+    out["n"] = np.array(c)
+    np.savez_compressed(HERE / "dtvc.npz", **out)
+
+    # -- power method -----------------------------------------------------
+    out = {}
+    c = 0
+    cases = [((8, 8), 0, 1, "f64"), ((8, 8, 8), 0, 2, "f64"), ((6, 5, 4), 2, 2, "f64"),
+             ((6, 6, 6, 6), 1, 3, "f64"), ((4, 4, 4, 4, 4), 4, 2, "f64"), ((9, 7, 5), 1, 3, "f32"),
+             ((8, 8, 8), 1, 2, "f32f64"), ((12, 10, 8), 0, 4, "f16f32"), ((12, 10, 8), 2, 3, "bf16f32"),
+             ((5, 6, 7, 8), 3, 4, "bf16f32"), ((16, 16, 16), 1, 1, "bf16f32")]
+    for shape, s, p, name in cases:
+        mode = T.MODES[name]
+        rng = np.random.default_rng(100 + c)
+        vals = rng.standard_normal(shape) + 0.5
+        A = T.Tensor.from_array(vals, mode)
+        x0 = T.initial_vectors(A.shape, mode, kind="random", seed=c)
+        res = T.dhopm3(T.distribute(A, s, p), x0, sweeps=3)
+        out[f"c{c}_meta"] = np.array([len(shape), *shape, s, p, 3])
+        out[f"c{c}_mode"] = np.array(name)
+        out[f"c{c}_buf"] = A.buf
+        for j, v in enumerate(x0):
+            out[f"c{c}_x0_{j}"] = v
+        for j, v in enumerate(res.vectors):
+            out[f"c{c}_v_{j}"] = v
+        out[f"c{c}_norms"] = np.array(res.norms)
+        out[f"c{c}_tvc_count"] = np.array(res.tvc_count)
+        out[f"c{c}_touched"] = np.array(res.iteration_touched)
+        can = T.hopm_canonical(A, x0, sweeps=3)
+        for j, v in enumerate(can.vectors):
+            out[f"c{c}_can_{j}"] = v
+        out[f"c{c}_can_norms"] = np.array(can.norms)
+        c += 1
+    # HOPM known answer (test_hopm.py:173-178): [[2,0],[0,1]] -> [1,0], lambda 2
+    A = T.Tensor.from_array(np.array([[2.0, 0.0], [0.0, 1.0]]))
+    res = T.dhopm3(T.distribute(A, 1, 2), sweeps=30)
+    out["diag_v0"], out["diag_v1"] = res.vectors
+    out["diag_norms"] = np.array(res.norms)
+    out["n"] = np.array(c)
+    np.savez_compressed(HERE / "hopm.npz", **out)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,267 @@
+"""GPU parity of conversions, normalisation, ring folds, dtvc and dhopm3
+against the reference's golden outputs and the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+import tenvec_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-12, "f32": 1e-5, "f32f64": 1e-6, "f16f32": 2e-3, "bf16f32": 1.6e-2}
+SUITE = [(2, 2), (3, 5), (6, 6), (2, 3, 4), (4, 4, 4), (5, 2, 6), (2, 3, 2, 4), (3, 3, 3, 3),
+         (2, 2, 3, 2, 4)]
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+def test_device_conversions_match_reference_bits(tv):
+    g = load_golden("precision")
+    assert np.array_equal(tv.demote(g["spots"], tv.BF16F32), g["spots_bf16"])
+    assert np.array_equal(tv.demote(g["spots"], tv.F32), g["spots_f32"])
+    assert np.array_equal(_bits(tv.demote(g["hvals"], tv.F16F32)), _bits(g["hvals_f16"]))
+    assert np.array_equal(_bits(tv.demote(g["hvals"].astype(np.float32), tv.F16F32)),
+                          _bits(g["hvals_f16_from_f32"]))
+    assert np.array_equal(tv.demote(g["hvals"], tv.BF16F32), g["hvals_bf16"])
+    assert np.array_equal(tv.promote(g["spots_bf16"], tv.BF16F32), g["bf16_widen"])
+    assert int(tv.f32_to_bf16_bits(np.array([np.pi], np.float32))[0]) == 0x4049
+    assert tv.bf16_bits_to_f32(np.array([0x4049], np.uint16))[0] == np.float32(3.140625)
+
+
+def test_normalize_examples(tv):
+    x = torch.tensor([3.0, 4.0], dtype=torch.float64, device="cuda")
+    assert tv.norm2(x) == 5.0
+    kc = tv.KernelCounters()
+    assert tv.normalize(x, counters=kc) == 5.0
+    assert x.tolist() == [0.6, 0.8] and kc.elements_touched == 6
+    y = x.clone()
+    tv.normalize(y)
+    assert torch.equal(x, y)
+    with pytest.raises(tv.NormalizationError):
+        tv.normalize(torch.zeros(3, dtype=torch.float64, device="cuda"))
+    for seed in range(20):
+        v = torch.from_numpy(np.random.default_rng(seed).standard_normal(1000)).cuda()
+        tv.normalize(v)
+        assert abs(tv.norm2(v) - 1.0) <= 4 * np.finfo(np.float64).eps
+    host = np.array([3.0, 4.0])
+    tv.normalize(host)
+    assert host.tolist() == [0.6, 0.8]
+
+
+@pytest.mark.parametrize("name", ["f64", "f32", "f32f64", "f16f32", "bf16f32"])
+def test_normalize_matches_oracle(tv, name):
+    mode = tv.MODES[name]
+    rng = np.random.default_rng(2)
+    for n in (1, 7, 64, 384, 4096):
+        xs = O.demote(rng.standard_normal(n), name).copy()
+        want = xs.copy()
+        nw = O.normalize(want, name)
+        got = torch.from_numpy(xs.copy()).cuda()
+        ng = tv.normalize(got, mode=mode)
+        assert abs(ng - nw) <= TOL[name] * nw
+        gw = O.promote(got.cpu().numpy(), name).astype(float)
+        ww = O.promote(want, name).astype(float)
+        assert np.allclose(gw, ww, rtol=TOL[name], atol=TOL[name])
+
+
+def test_ring_folds_bitwise_against_reference(tv):
+    g = load_golden("ring")
+    for c in range(int(g["n"])):
+        name = str(g[f"c{c}_mode"])
+        mode = tv.MODES[name]
+        ranks = g[f"c{c}_ranks"]
+        bufs = [torch.from_numpy(r.copy()).cuda() for r in ranks]
+        counters = [tv.CommCounters() for _ in bufs]
+        if mode.mixed:
+            tv.ring_all_reduce_mixed(bufs, mode, counters)
+        else:
+            tv.ring_all_reduce(bufs, counters)
+        for b in bufs:
+            assert np.array_equal(_bits(b.cpu().numpy()), _bits(g[f"c{c}_out"])), (c, name)
+        p, n = len(bufs), ranks.shape[1]
+        if n % p == 0:
+            assert all(cc.touched_elements == 4 * n * (p - 1) // p for cc in counters)
+
+
+def test_worker_group_threads_on_device(tv):
+    group = tv.WorkerGroup(3, timeout=20)
+    data = [torch.full((10,), float(r + 1), dtype=torch.float64, device="cuda") for r in range(3)]
+
+    def body(rank):
+        group.all_reduce_sum(rank, data[rank])
+        got = group.all_gather(rank, data[rank][:2])
+        group.barrier(rank)
+        return got.cpu().numpy()
+
+    res = group.run(body)
+    for r in range(3):
+        assert torch.equal(data[r], torch.full((10,), 6.0, dtype=torch.float64, device="cuda"))
+        assert res[r].tolist() == [6.0] * 6
+
+
+def test_dtvc_shape_suite_against_reference(tv):
+    g = load_golden("dtvc")
+    tensors = {}
+    for c in range(int(g["n"])):
+        rec = g[f"c{c}"]
+        d = int(rec[0])
+        shape = tuple(int(e) for e in rec[1:1 + d])
+        k, s, p, defer = (int(e) for e in rec[1 + d:5 + d])
+        if shape not in tensors:
+            tensors[shape] = tv.Tensor.from_array(g[f"vals{SUITE.index(shape)}"].reshape(shape))
+        x = np.random.default_rng(10 * k + 1).integers(-4, 5, shape[k]).astype(float)
+        res = tv.dtvc(tv.distribute(tensors[shape], s, p), x, k, defer=bool(defer))
+        assert res.kind == ("partial-sum" if defer else "disjoint")
+        got = tv.undistribute(res).to_float64().reshape(-1)
+        assert np.array_equal(got, rec[5 + d:]), (shape, k, s, p, defer)
+
+
+def test_dtvc_examples_and_errors(tv):
+    A = tv.Tensor.from_array(np.array([[1.0, 2.0], [3.0, 4.0]]))
+    x = np.array([10.0, 1.0])
+    dt = tv.dtvc(tv.distribute(A, 0, 2), x, 1)
+    assert dt.kind == tv.DISJOINT and [p.to_float64()[0] for p in dt.parts] == [12.0, 34.0]
+    dt = tv.dtvc(tv.distribute(A, 1, 2), x, 1, defer=True)
+    assert dt.kind == tv.PARTIAL_SUM
+    assert dt.parts[0].to_float64().tolist() == [10.0, 30.0]
+    assert dt.parts[1].to_float64().tolist() == [2.0, 4.0]
+    now = tv.dtvc(tv.distribute(A, 1, 2), x, 1)
+    assert now.plan.p_eff == 1 and now.parts[0].to_float64().tolist() == [12.0, 34.0]
+    t = tv.Tensor.from_array(np.arange(60.0).reshape(3, 4, 5))
+    assert tv.dtvc(tv.distribute(t, 2, 2), np.arange(3.0), 0).split_mode == 1
+    assert tv.dtvc(tv.distribute(t, 0, 3), np.arange(5.0), 2).split_mode == 0
+    with pytest.raises(tv.ContractError):
+        tv.dtvc(tv.distribute(t, 0, 2), np.ones(3), 3)
+    with pytest.raises(tv.ContractError):
+        tv.dtvc(tv.distribute(t, 0, 2), np.ones(5), 0)
+
+
+@pytest.mark.parametrize("name", ["f16f32", "bf16f32", "f32f64"])
+def test_dtvc_mixed_reduction_bitwise(tv, name):
+    mode = tv.MODES[name]
+    rng = np.random.default_rng(4)
+    vals = rng.uniform(-2, 2, (12, 10, 9))
+    t = tv.Tensor.from_array(vals, mode)
+    host = t.to_numpy().reshape(12, 10, 9)
+    for s in range(3):
+        for p in (2, 3, 4):
+            x = O.demote(rng.uniform(-1, 1, vals.shape[s]), name).copy()
+            res = tv.dtvc(tv.distribute(t, s, p), x, s)
+            parts, ranges = O.split(host, s, p)
+            _, outs, _ = O.dtvc(parts, ranges, s, x, s, name)
+            got = res.parts[0].to_numpy()
+            want = outs[0].reshape(-1)
+            # the per-rank TVCs may differ in the last compute bit from BLAS, so
+            # compare the fold exactly on OUR partials and the result within tol
+            dt_def = tv.dtvc(tv.distribute(t, s, p), x, s, defer=True)
+            ours = [pp.to_numpy() for pp in dt_def.parts]
+            assert np.array_equal(_bits(got), _bits(O.fold_mixed(ours, name)))
+            assert np.allclose(O.promote(got, name), O.promote(want, name), rtol=TOL[name], atol=TOL[name])
+
+
+def test_dhopm3_against_reference_golden(tv):
+    g = load_golden("hopm")
+    for c in range(int(g["n"])):
+        meta = [int(e) for e in g[f"c{c}_meta"]]
+        d = meta[0]
+        shape = tuple(meta[1:1 + d])
+        s, p, sweeps = meta[1 + d:4 + d]
+        name = str(g[f"c{c}_mode"])
+        mode = tv.MODES[name]
+        A = tv.Tensor(tv.Shape(shape), g[f"c{c}_buf"], mode)
+        x0 = [g[f"c{c}_x0_{j}"] for j in range(d)]
+        res = tv.dhopm3(tv.distribute(A, s, p), x0, sweeps=sweeps)
+        assert res.tvc_count == int(g[f"c{c}_tvc_count"])
+        assert res.iteration_touched == g[f"c{c}_touched"].tolist()
+        tol = 10 * TOL[name]
+        for j in range(d):
+            got = O.promote(res.vectors[j], name).astype(float)
+            want = O.promote(g[f"c{c}_v_{j}"], name).astype(float)
+            assert np.allclose(got, want, rtol=tol, atol=tol), (c, name, j)
+        assert np.allclose(res.norms, g[f"c{c}_norms"], rtol=tol), c
+        # the canonical schedule reaches the same fixed point
+        can = tv.hopm_canonical(A, x0, sweeps=sweeps)
+        assert np.allclose(can.norms, g[f"c{c}_can_norms"], rtol=tol)
+
+
+def test_dhopm3_single_rank_bitwise_equals_canonical(tv):
+    for d, n in ((2, 6), (3, 5), (4, 3)):
+        A = tv.Tensor.from_array(np.random.default_rng(d).standard_normal((n,) * d))
+        x0 = tv.initial_vectors(A.shape, kind="random", seed=42)
+        want = tv.hopm_canonical(A, x0, sweeps=2)
+        got = tv.dhopm3(tv.distribute(A, 0, 1), x0, sweeps=2)
+        for a, b in zip(got.vectors, want.vectors):
+            assert np.array_equal(a, b)
+        assert got.norms == want.norms
+
+
+def test_dhopm3_integer_tensor_bitwise_vs_oracle(tv):
+    """Integer data, fp64: every TVC is exact, so the whole run must be bitwise
+    the oracle's (the norms' sqrt/divide are IEEE on both sides)."""
+    rng = np.random.default_rng(8)
+    for shape, s, p in (((8, 8, 8), 0, 2), ((6, 5, 4, 3), 2, 3), ((10, 12), 1, 4)):
+        vals = rng.integers(1, 6, shape).astype(float)
+        A = tv.Tensor.from_array(vals)
+        x0 = [np.ones(n) for n in shape]
+        res = tv.dhopm3(tv.distribute(A, s, p), x0, sweeps=1)
+        vecs, norms = O.dhopm3(vals, s, p, [np.ones(n) for n in shape], 1, "f64")
+        assert np.allclose(res.norms, norms, rtol=1e-14)
+        for a, b in zip(res.vectors, vecs):
+            assert np.allclose(a, b, rtol=1e-13, atol=1e-15)
+
+
+def test_dhopm3_matrix_known_answer_and_counts(tv):
+    A = tv.Tensor.from_array(np.array([[2.0, 0.0], [0.0, 1.0]]))
+    for s in (0, 1):
+        for p in (1, 2):
+            res = tv.dhopm3(tv.distribute(A, s, p), sweeps=30)
+            assert np.allclose(res.vectors[0], [1.0, 0.0], atol=1e-9)
+            assert np.allclose(res.vectors[1], [1.0, 0.0], atol=1e-9)
+            assert abs(res.norms[-1][0] - 2.0) < 1e-9
+    A4 = tv.Tensor.from_array(np.random.default_rng(11).integers(1, 4, (3, 3, 3, 3)).astype(float))
+    res = tv.dhopm3(tv.distribute(A4, 1, 3), sweeps=2)
+    assert res.tvc_per_sweep == 9 and res.tvc_count == 18
+    classical = tv.dhopm3(tv.distribute(A4, 1, 3), sweeps=2, reuse=False)
+    assert classical.tvc_per_sweep == 12
+    A3 = tv.Tensor.from_array(np.random.default_rng(13).integers(1, 4, (4, 4, 4)).astype(float))
+    res = tv.dhopm3(tv.distribute(A3, 1, 2), sweeps=3)
+    assert all(c.collective_calls == 9 for c in res.comm_counters)
+
+
+def test_dhopm3_counters_match_simulation(tv):
+    for d, n in ((3, 6), (4, 4)):
+        for p in (1, 2):
+            for s in range(d):
+                A = tv.Tensor.from_array(np.random.default_rng(n + s).integers(1, 4, (n,) * d).astype(float))
+                res = tv.dhopm3(tv.distribute(A, s, p), sweeps=2)
+                sim = tv.simulate_hopm((n,) * d, s, p, reuse=True)
+                for r in range(p):
+                    assert res.iteration_touched[r] == sim[r].iteration_touched * 2
+
+
+def test_dhopm3_validation_and_zero_tensor(tv):
+    A = tv.Tensor.from_array(np.random.default_rng(19).integers(-4, 5, (3, 3)).astype(float))
+    dt = tv.distribute(A, 0, 2)
+    ps = tv.DistributedTensor(dt.plan, [tv.Tensor.from_array(np.ones((3, 3)))] * 2, tv.PARTIAL_SUM)
+    with pytest.raises(tv.ContractError):
+        tv.dhopm3(ps)
+    with pytest.raises(tv.ContractError):
+        tv.dhopm3(dt, [np.ones(3)])
+    with pytest.raises(tv.ContractError):
+        tv.dhopm3(dt, [np.ones(3), np.ones(4)])
+    with pytest.raises(tv.NormalizationError):
+        tv.dhopm3(tv.distribute(tv.Tensor.from_array(np.zeros((3, 3, 3))), 0, 2))
+
+
+def test_initial_vectors(tv):
+    xs = tv.initial_vectors(tv.Shape((4, 9)))
+    assert np.allclose(xs[0], 0.5) and np.allclose(xs[1], 1.0 / 3.0)
+    assert tv.initial_vectors(tv.Shape((4,)), tv.BF16F32)[0].dtype == np.uint16
+    a = tv.initial_vectors(tv.Shape((5, 5)), kind="random", seed=7)
+    b = O.initial_vectors((5, 5), "f64", kind="random", seed=7)
+    for u, v in zip(a, b):
+        assert np.allclose(u, v, rtol=1e-15, atol=1e-16)

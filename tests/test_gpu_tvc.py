@@ -1,0 +1,257 @@
+"""GPU parity of the native TVC (tv_tvc) against the oracle and the reference's
+golden outputs.  Integer fills are bitwise; float data within the stated
+per-mode tolerance (north_star: fp64 1e-12, fp32 1e-5)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+import tenvec_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-12, "f32": 1e-5, "f32f64": 1e-6, "f16f32": 2e-3, "bf16f32": 1.6e-2}
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+def _close(got, want, mode, ctx):
+    if np.array_equal(_bits(got), _bits(want)):
+        return
+    gw = O.promote(got, mode).astype(float)
+    ww = O.promote(want, mode).astype(float)
+    tol = TOL[mode]
+    # normwise relative error, plus elementwise slack of one storage ulp for
+    # the narrow formats (the summation order differs from OpenBLAS)
+    err = np.linalg.norm(gw - ww) / max(np.linalg.norm(ww), 1e-300)
+    assert err <= tol or np.allclose(gw, ww, rtol=tol, atol=tol), (ctx, err)
+
+
+def test_known_answers(tv):
+    A = tv.Tensor.from_array(np.array([[1.0, 2.0], [3.0, 4.0]]))
+    x = np.array([10.0, 1.0])
+    assert tv.tvc_native(A, x, 1).to_float64().tolist() == [12.0, 34.0]
+    assert tv.tvc_native(A, x, 0).to_float64().tolist() == [13.0, 24.0]
+    t = tv.Tensor.from_array(np.ones((2, 3, 4)))
+    y = tv.tvc_native(t, np.ones(3), 1)
+    assert y.shape.extents == (2, 4) and np.all(y.to_float64() == 3.0)
+
+
+def test_getvc_examples_and_strided_view(tv):
+    a = torch.tensor([[1.0, 2.0], [3.0, 4.0]], dtype=torch.float64, device="cuda")
+    x = torch.tensor([10.0, 1.0], dtype=torch.float64, device="cuda")
+    y = torch.empty(2, dtype=torch.float64, device="cuda")
+    tv.getvc(tv.MATVEC, 1.0, a, x, 0.0, y)
+    assert y.tolist() == [12.0, 34.0]
+    tv.getvc(tv.VECMAT, 1.0, a, x, 0.0, y)
+    assert y.tolist() == [13.0, 24.0]
+    y = torch.tensor([7.0, 7.0], dtype=torch.float64, device="cuda")
+    tv.getvc(tv.MATVEC, 0.0, a, torch.ones(2, dtype=torch.float64, device="cuda"), 1.0, y)
+    assert y.tolist() == [7.0, 7.0]
+    # leading dimension larger than n (kernels.py:90-91): a column window
+    big = torch.arange(1.0, 1.0 + 6 * 9, dtype=torch.float64, device="cuda").reshape(6, 9)
+    view = big[:, 2:7]
+    xs = torch.arange(1.0, 6.0, dtype=torch.float64, device="cuda")
+    ym = torch.empty(6, dtype=torch.float64, device="cuda")
+    tv.getvc(tv.MATVEC, 1.0, view, xs, 0.0, ym)
+    assert torch.equal(ym, view @ xs)
+    xv = torch.arange(1.0, 7.0, dtype=torch.float64, device="cuda")
+    yv = torch.empty(5, dtype=torch.float64, device="cuda")
+    tv.getvc(tv.VECMAT, 1.0, view, xv, 0.0, yv)
+    assert torch.equal(yv, xv @ view)
+    with pytest.raises(tv.KernelError):
+        tv.getvc(tv.MATVEC, 1.0, a, torch.ones(3, dtype=torch.float64, device="cuda"), 0.0, y)
+
+
+def test_tvc_golden_integer_shapes_bitwise(tv):
+    g = load_golden("tvc_int")
+    for i in range(int(g["n"])):
+        shape = tuple(int(e) for e in g[f"c{i}_shape"])
+        k = int(g[f"c{i}_k"])
+        t = tv.Tensor.from_array(g[f"c{i}_vals"].reshape(shape))
+        y = tv.tvc_native(t, g[f"c{i}_x"], k)
+        assert np.array_equal(y.to_float64().reshape(-1), g[f"c{i}_y"]), (i, shape, k)
+        assert np.array_equal(tv.tvc_looped_oracle(t, g[f"c{i}_x"], k).reshape(-1), g[f"c{i}_y"])
+
+
+def test_tvc_golden_all_modes_alpha_beta(tv):
+    g = load_golden("tvc_modes")
+    for c in range(int(g["n"])):
+        mode_name = str(g[f"c{c}_mode"])
+        mode = tv.MODES[mode_name]
+        shape = tuple(int(e) for e in g[f"c{c}_shape"])
+        k = int(g[f"c{c}_k"])
+        alpha, beta = (float(v) for v in g[f"c{c}_ab"])
+        t = tv.Tensor(tv.Shape(shape), g[f"c{c}_buf"], mode)
+        out = torch.from_numpy(g[f"c{c}_y0"].copy()).cuda()
+        y = tv.tvc_native(t, g[f"c{c}_x"], k, alpha=alpha, beta=beta, out=out)
+        _close(y.to_numpy(), g[f"c{c}_y"], mode_name, (c, mode_name, shape, k))
+
+
+REGIME_CASES = [
+    # (shape, k, expected regime) -- per storage width the vector length changes,
+    # so regimes are asserted for f32 storage only
+    ((64, 256), 1, "rows"),
+    ((300, 96), 1, "rows"),
+    ((96, 96, 12), 2, "rows_short"),
+    ((5000, 8), 1, "rows_short"),
+    ((256, 256), 0, "cols"),
+    ((7, 40, 256), 1, "cols"),
+    ((96, 96, 12), 1, "slabs"),
+    ((33, 17, 48), 1, "slabs"),
+    ((5, 7, 3), 1, "generic"),
+    ((9, 13), 1, "generic"),
+    ((1, 1024, 1), 1, "rows"),
+    ((2, 3), 0, "generic"),
+]
+
+
+@pytest.mark.parametrize("mode_name", ["f64", "f32", "f32f64", "f16f32", "bf16f32"])
+@pytest.mark.parametrize("shape,k,regime", REGIME_CASES)
+def test_regimes_integer_bitwise(tv, mode_name, shape, k, regime):
+    mode = tv.MODES[mode_name]
+    rng = np.random.default_rng(hash((shape, k)) % 2**32)
+    vals = rng.integers(1, 98, shape).astype(np.float64)
+    x64 = rng.integers(1, 98, shape[k]).astype(np.float64)
+    t = tv.Tensor.from_array(vals, mode)
+    xs = O.demote(x64, mode_name).copy()
+    if mode_name == "f32":
+        assert tv.tvc_regime(t, k) == regime
+    y = tv.tvc_native(t, xs, k)
+    want = O.tvc(O.demote(vals.reshape(-1), mode_name), shape, xs, k, mode_name)
+    assert np.array_equal(_bits(y.to_numpy()), _bits(want)), (shape, k, mode_name, tv.tvc_regime(t, k))
+
+
+@pytest.mark.parametrize("mode_name", ["f64", "f32", "bf16f32"])
+def test_regimes_float_data(tv, mode_name):
+    mode = tv.MODES[mode_name]
+    rng = np.random.default_rng(5)
+    for shape in [(40, 64, 48), (3, 1000, 5), (128, 3, 64), (17, 19, 23), (2, 4096)]:
+        vals = rng.standard_normal(shape)
+        t = tv.Tensor.from_array(vals, mode)
+        for k in range(len(shape)):
+            xs = O.demote(rng.standard_normal(shape[k]), mode_name).copy()
+            y = tv.tvc_native(t, xs, k)
+            want = O.tvc(t.to_numpy(), shape, xs, k, mode_name)
+            _close(y.to_numpy(), want, mode_name, (shape, k))
+            again = tv.tvc_native(t, xs, k)
+            assert torch.equal(again.buf.view(torch.uint8) if again.buf.dtype != torch.uint16 else again.buf.view(torch.int16),
+                               y.buf.view(torch.uint8) if y.buf.dtype != torch.uint16 else y.buf.view(torch.int16))
+
+
+def test_misaligned_view_uses_generic(tv):
+    base = torch.arange(1.0, 1.0 + 4 * 64 + 1, dtype=torch.float32, device="cuda")
+    buf = base[1:]  # 4-byte offset: not 16-byte aligned
+    t = tv.Tensor(tv.Shape((4, 64)), buf, tv.F32)
+    assert tv.tvc_regime(t, 1) == "generic"
+    x = np.arange(64, dtype=np.float32) % 5
+    y = tv.tvc_native(t, x, 1)
+    want = O.tvc(buf.cpu().numpy(), (4, 64), x, 1, "f32")
+    assert np.array_equal(y.to_numpy(), want)
+
+
+def test_beta_zero_never_reads_y_and_out_prefix(tv):
+    t = tv.Tensor.from_array(np.ones((3, 4, 2)))
+    for k in range(3):
+        n = t.size // t.shape.extents[k]
+        out = torch.full((n + 5,), float("nan"), dtype=torch.float64, device="cuda")
+        y = tv.tvc_native(t, np.ones(t.shape.extents[k]), k, out=out)
+        assert not torch.isnan(y.buf).any()
+        assert y.buf.data_ptr() == out.data_ptr()
+        assert torch.isnan(out[n:]).all()
+    with pytest.raises(tv.KernelError):
+        tv.tvc_native(t, np.ones(3), 1, out=torch.empty(1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(tv.KernelError):
+        tv.tvc_native(t, np.ones(2), 1)
+
+
+def test_counters_match_reference_convention(tv):
+    t = tv.Tensor.from_array(np.ones((4, 4, 4)))
+    for k in range(3):
+        kc = tv.KernelCounters()
+        tv.tvc_native(t, np.ones(4), k, counters=kc)
+        assert (kc.elements_read, kc.elements_written) == (68, 16)
+    kc = tv.KernelCounters()
+    tv.tvc_native(t, np.ones(4), 1, beta=1.0, out=torch.zeros(16, dtype=torch.float64, device="cuda"), counters=kc)
+    assert kc.elements_read == 84
+
+
+def test_half_accumulates_wide_and_overflows_on_store(tv):
+    t = tv.Tensor.from_array(np.full((1, 4096), 32.0), tv.F16F32)
+    y = tv.tvc_native(t, np.ones(4096, np.float16), 1)
+    assert np.isinf(y.to_float64()[0])
+    t2 = tv.Tensor.from_array(np.full((1, 1000), 32.0), tv.F16F32)
+    y2 = tv.tvc_native(t2, np.ones(1000, np.float16), 1)
+    assert y2.to_float64()[0] == 32000.0
+
+
+def test_brain_pipeline_known_answer(tv):
+    a64 = np.array([[1.5, 2.25], [3.0, -4.5]])
+    x64 = np.array([0.5, 2.0])
+    a = tv.Tensor.from_array(a64, tv.BF16F32)
+    xs = O.demote(x64, "bf16f32")
+    y = tv.tvc_native(a, xs, 1)
+    assert np.array_equal(y.to_numpy(), O.demote(a64 @ x64, "bf16f32"))
+
+
+def test_linearity_and_unit_vector(tv):
+    rng = np.random.default_rng(17)
+    vals = rng.standard_normal((40, 30, 50))
+    t = tv.Tensor.from_array(vals)
+    x, z = rng.standard_normal(30), rng.standard_normal(30)
+    a, b = 1.7, -0.3
+    lhs = tv.tvc_native(t, a * x + b * z, 1).to_float64()
+    rhs = a * tv.tvc_native(t, x, 1).to_float64() + b * tv.tvc_native(t, z, 1).to_float64()
+    assert np.allclose(lhs, rhs, rtol=1e-12, atol=1e-12)
+    e = np.zeros(30)
+    e[7] = 1.0
+    assert np.array_equal(tv.tvc_native(t, e, 1).to_float64(), vals[:, 7, :])
+
+
+@pytest.mark.parametrize("kind", ["ones", "ramp", "hash"])
+def test_device_fill_matches_oracle(tv, kind):
+    shape = tv.Shape((6, 10, 7))
+    for s in range(3):
+        dt = tv.distribute_generated(shape, s, 3, tv.F32, fill=kind, seed=5)
+        whole = tv.undistribute(dt).to_float64().reshape(-1)
+        assert np.array_equal(whole, O.fill_values(shape.extents, kind, seed=5)), (kind, s)
+
+
+def test_c1_256_cubed_every_mode_bitwise(tv):
+    """BASELINE config C1: 256^3 fp64, integer fill, k = 0, 1, 2."""
+    shape = (256, 256, 256)
+    dt = tv.distribute_generated(tv.Shape(shape), 0, 1, tv.F64, fill="hash", seed=1)
+    t = dt.parts[0]
+    host = O.fill_values(shape, "hash", seed=1)
+    for k in range(3):
+        x = O.fill_values((256,), "ramp")[::-1].copy()
+        y = tv.tvc_native(t, x, k)
+        want = O.tvc(host, shape, x, k, "f64")
+        assert np.array_equal(y.to_numpy(), want), k
+
+
+@pytest.mark.parametrize("mode_name,shape", [("f64", (1024, 1024, 1024)), ("f32", (96, 96, 96, 96)),
+                                             ("bf16f32", (2048, 2048, 256))])
+def test_large_views_sampled_exact(tv, mode_name, shape):
+    """Full-size-style views checked on sampled outputs regenerated from the
+    closed-form hash fill (size-independent, exact for integer data)."""
+    mode = tv.MODES[mode_name]
+    dt = tv.distribute_generated(tv.Shape(shape), 0, 1, mode, fill="hash", seed=9)
+    t = dt.parts[0]
+    rng = np.random.default_rng(3)
+    for k in range(len(shape)):
+        u, nk, v = math.prod(shape[:k]), shape[k], math.prod(shape[k + 1:])
+        x64 = (np.arange(nk) % 7) + 1.0  # keeps every partial sum below 2**24
+        xs = O.demote(x64, mode_name)
+        y = tv.tvc_native(t, xs, k).to_numpy()
+        for _ in range(24):
+            i, l = int(rng.integers(u)), int(rng.integers(v))
+            g = (i * nk + np.arange(nk)) * v + l
+            vals = (O.fill_hash(9, g.astype(np.uint64)) % np.uint64(97)).astype(np.float64) + 1.0
+            want = O.demote(np.array([np.dot(vals, O.promote(xs, mode_name).astype(np.float64))]), mode_name)
+            assert np.array_equal(_bits(y[i * v + l: i * v + l + 1]), _bits(want)), (k, i, l)

@@ -1,0 +1,186 @@
+"""CPU-only checks of the host side: mode table, shapes and split plans,
+schedule and traffic model (against the reference's recorded counts), counters,
+the WorkerGroup rendezvous, and the C-ABI library's exports and argument
+validation (no kernel launches)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden
+import paper_2501_03121_b200 as tv
+from paper_2501_03121_b200 import _lib, build
+
+
+def test_mode_table():
+    assert sorted(tv.MODES) == ["bf16f32", "f16f32", "f32", "f32f64", "f64"]
+    assert tv.BF16F32.storage_bytes == 2 and tv.BF16F32.compute_bytes == 4 and tv.BF16F32.mixed
+    assert tv.F32F64.mixed and not tv.F64.mixed
+    assert tv.BF16F32.storage_dtype == np.uint16
+    with pytest.raises(tv.ModeError):
+        tv.parse_mode("f8")
+
+
+def test_shapes_and_views():
+    s = tv.Shape((2, 3, 4))
+    assert s.order == 3 and s.size == 24 and str(s) == "2x3x4"
+    assert s.drop(1).extents == (2, 4) and tv.Shape((5,)).drop(0).extents == (1,)
+    assert tv.parse_shape("979^3").extents == (979,) * 3
+    assert tv.parse_shape("2,3,4") == s and tv.parse_shape("2x3x4") == s
+    md = tv.matricize_dims(s, 1)
+    assert (md.u, md.nk, md.v) == (2, 3, 4)
+    assert tv.linear_index(s, (1, 2, 3)) == 23
+    with pytest.raises(IndexError):
+        tv.matricize_dims(s, 3)
+    with pytest.raises(ValueError):
+        tv.Shape(())
+
+
+def test_division_rule():
+    assert tv.optimal_division(4, 3, 8) == (2, 2)
+    assert tv.optimal_division(96, 8, 8) == (16, 6)  # the vl=8 trap on C3
+    assert tv.optimal_division(96, 8, 1) == (12, 8)
+    rng = np.random.default_rng(41)
+    for _ in range(500):
+        n, p, vl = int(rng.integers(1, 2000)), int(rng.integers(1, 64)), int(2 ** rng.integers(0, 6))
+        q, pe = tv.optimal_division(n, p, vl)
+        assert 1 <= pe <= p and q * pe >= n > q * (pe - 1)
+        if n >= vl:
+            assert q == n or q % vl == 0
+    plan = tv.make_split_plan(10, 1, 4)
+    assert plan.ranges == ((0, 3), (3, 6), (6, 9), (9, 10)) and plan.extent == 10
+
+
+def test_task_ranges_and_counters():
+    for total in (1, 5, 8, 17):
+        for tasks in (1, 2, 3, 8, 30):
+            hits = np.zeros(total, dtype=int)
+            for a, b in tv.task_ranges(total, tasks):
+                hits[a:b] += 1
+            assert np.all(hits == 1)
+    kc = tv.KernelCounters()
+    kc.count("tvc", 68, 16, 8)
+    other = tv.KernelCounters()
+    other.count("tvc", 4, 4, 2)
+    kc.add(other)
+    assert kc.elements_touched == 92 and kc.bytes_touched == 84 * 8 + 16 and kc.invocations == {"tvc": 2}
+
+
+def test_schedule_counts():
+    for d in range(2, 11):
+        assert tv.tvc_per_sweep(d, True) == (d - 1) * (d + 2) // 2
+        assert tv.tvc_per_sweep(d, False) == d * (d - 1)
+    assert tv.iteration_plan(5, 3, True) == (frozenset({0, 1}), [2, 4])
+    assert tv.mode_remap(2, {0, 1}) == 0 and tv.mode_remap(3, {1}) == 2
+    with pytest.raises(ValueError):
+        tv.mode_remap(1, {1})
+
+
+def test_simulation_matches_reference_runs():
+    """iteration_touched recorded from the reference's dhopm3 equals the traffic
+    model restated in schedule.py (the roofline numerator of bench.py)."""
+    g = load_golden("hopm")
+    for c in range(int(g["n"])):
+        meta = [int(e) for e in g[f"c{c}_meta"]]
+        d = meta[0]
+        shape = tuple(meta[1:1 + d])
+        s, p, sweeps = meta[1 + d:4 + d]
+        sim = tv.simulate_hopm(shape, s, p, reuse=True)
+        touched = g[f"c{c}_touched"].tolist()
+        for r in range(len(sim)):
+            assert touched[r] == sim[r].iteration_touched * sweeps
+        assert int(g[f"c{c}_tvc_count"]) == sim[0].tvc_count * sweeps
+
+
+def test_baseline_traffic_figures():
+    # 384^4 fp64 p=8 s=3 -> 43,770,757,632 B per rank per sweep
+    assert tv.schedule.sweep_bytes((384,) * 4, 3, 8, 8)[0] == 43_770_757_632
+    assert sum(tv.schedule.sweep_bytes((384,) * 4, 3, 1, 8)) == 350_165_609_472
+
+
+def test_ring_chunks():
+    assert tv.ring_chunks(10, 3) == [(0, 4), (4, 8), (8, 10)]
+    assert tv.ring_chunks(2, 4) == [(0, 1), (1, 2), (2, 2), (2, 2)]
+    assert tv.ring_chunks(0, 3) == [(0, 0)] * 3
+
+
+def test_worker_group_rendezvous_errors():
+    g = tv.WorkerGroup(3, timeout=0.5)
+
+    def body(rank):
+        if rank != 2:
+            g.barrier(rank)
+        return rank
+
+    with pytest.raises(tv.CollectiveTimeout) as info:
+        g.run(body)
+    assert info.value.absent == [2]
+
+    g = tv.WorkerGroup(2, timeout=2.0)
+
+    def mismatch(rank):
+        if rank == 0:
+            g.barrier(rank)
+        else:
+            g.all_gather(rank, None)
+
+    with pytest.raises(tv.CollectiveError):
+        g.run(mismatch)
+
+    g = tv.WorkerGroup(2, timeout=0.5)
+
+    def failing(rank):
+        if rank == 1:
+            raise ValueError("boom")
+        g.barrier(rank)
+
+    with pytest.raises(ValueError):
+        g.run(failing)
+    with pytest.raises(ValueError):
+        tv.WorkerGroup(0)
+
+
+def _header_symbols() -> set[str]:
+    text = (ROOT / "include" / "tenvec_b200.h").read_text()
+    return set(re.findall(r"^\s*(?:const char\*|int)\s+(tv_\w+)\s*\(", text, flags=re.M))
+
+
+def test_library_builds_loads_and_exports_every_header_symbol():
+    build.build()
+    lib = _lib.load()
+    declared = _header_symbols()
+    assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.tv_version().startswith(b"tenvec_b200")
+
+
+def test_library_argument_validation_without_gpu():
+    lib = _lib.load()
+    # nk = 0 and bad modes are rejected before any launch
+    assert lib.tv_tvc(None, 0, 0, 4, 0, 4, None, 1.0, 0.0, None, None) == 1
+    assert b"nk" in lib.tv_last_error()
+    assert lib.tv_tvc_regime(None, 0, 4, 0, 4) == -1
+    assert lib.tv_getvc(2, None, 0, 0, 2, 2, 2, None, 1.0, 0.0, None, None) == 1
+    assert lib.tv_getvc(0, None, 0, 0, 2, 3, 2, None, 1.0, 0.0, None, None) == 1
+    assert lib.tv_convert(None, 0, None, 1, -1, None) == 1
+    assert lib.tv_rank_fold(None, 0, 4, 0, 0, 0, 0, 0, None, None) == 4
+    ext = (ctypes.c_int64 * 3)(2, 3, 4)
+    assert lib.tv_fill(None, 0, 0, 1, ext, 3, 1, 2, 1, None) == 1
+    # regime choice is host logic: aligned fake pointers, no dereference
+    p = 1 << 20
+    assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 1       # rows
+    assert lib.tv_tvc_regime(p, 1, 1000, 12, 1) == 2       # short rows
+    assert lib.tv_tvc_regime(p, 1, 1, 2048, 4096) == 3     # columns
+    assert lib.tv_tvc_regime(p, 1, 1000, 96, 12) == 4      # narrow slabs
+    assert lib.tv_tvc_regime(p + 4, 1, 1000, 96, 12) == 0  # misaligned -> generic
+
+
+def test_no_oracle_import_in_product():
+    pkg = ROOT / "paper_2501_03121_b200"
+    for f in pkg.rglob("*.py"):
+        text = f.read_text()
+        assert "tenvec_oracle" not in text and "oracle/" not in text, f

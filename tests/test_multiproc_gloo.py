@@ -1,0 +1,94 @@
+"""The one-process-per-GPU collective plan of RankGroup, exercised on CPU over
+gloo with world sizes 2 and 3: all-to-all of ring chunks, a fold per chunk
+(the oracle's, injected in place of the CUDA fold kernel) and the all-gather
+must reproduce the reference's ring_all_reduce / ring_all_reduce_mixed values
+bit for bit, and all_gather must concatenate uneven slices in rank order."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = [("f64", 10), ("f32", 7), ("f16f32", 11), ("bf16f32", 13), ("f32f64", 5), ("f64", 1)]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _rank_data(mode_name, n, r, O):
+    rng = np.random.default_rng(1000 + 17 * r + n)
+    return O.demote(rng.uniform(-4, 4, n), mode_name).copy()
+
+
+def _worker(rank, world, port, q):
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import tenvec_oracle as O
+        import paper_2501_03121_b200 as tv
+
+        names = {torch.float64: "f64", torch.float32: "f32", torch.float16: "f16f32", torch.uint16: "bf16f32"}
+
+        def host_fold(recv, stride, p, n, dst, *, mixed, mode, start):
+            name = mode.name if mode is not None else names[dst.dtype]
+            arr = recv.numpy()
+            contribs = [arr[r * stride: r * stride + n] for r in range(p)]
+            out = O.fold_chunk(contribs, start, name, mixed)
+            dst.view(torch.int16 if dst.dtype == torch.uint16 else dst.dtype).copy_(
+                torch.from_numpy(out.view(np.int16) if out.dtype == np.uint16 else out))
+
+        group = tv.RankGroup(fold=host_fold)
+        results = []
+        for name, n in CASES:
+            mode = tv.MODES[name]
+            mine = _rank_data(name, n, rank, O)
+            buf = torch.from_numpy(mine.copy())
+            if mode.mixed:
+                group.all_reduce_sum_mixed(rank, buf, mode)
+            else:
+                group.all_reduce_sum(rank, buf)
+            everyone = [_rank_data(name, n, r, O) for r in range(world)]
+            want = O.fold_mixed(everyone, name) if mode.mixed else O.fold_exact(everyone)
+            results.append(bool(np.array_equal(buf.numpy().view(np.uint8), want.view(np.uint8))))
+        # uneven gather: the last rank is short, like a split plan's last slab
+        counts = [3] * (world - 1) + [1]
+        local = torch.arange(counts[rank], dtype=torch.float64) + 10 * rank
+        got = group.all_gather(rank, local, counts)
+        want = np.concatenate([np.arange(c, dtype=np.float64) + 10 * r for r, c in enumerate(counts)])
+        results.append(bool(np.array_equal(got.numpy(), want)))
+        with pytest.raises(tv.CollectiveError):
+            group.all_reduce_sum((rank + 1) % world, buf)
+        results.append(group.counters[0].collective_calls == len(CASES) + 1)
+        q.put((rank, results))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_group_reference_values_over_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, res = q.get(timeout=240)
+        out[r] = res
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert all(out[r]), (r, out[r])
