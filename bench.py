@@ -317,6 +317,7 @@ def run_ours(args) -> dict | None:
 
     # e2e: the same steps with the slab uploaded from pinned host memory and the
     # outputs read back, through the same public API
+    read_gbs = read_stream_gbs(part.buf)
     e2e = run_e2e_sweep(args, tv, dt, part, xs, s, world, rank, group, job_bytes_step)
 
     if rank != 0:
@@ -348,6 +349,8 @@ def run_ours(args) -> dict | None:
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
                      if not peaks.get("_fallback") else "fallback 6650 GB/s"},
         "modes": modes,
+        "read_stream_gbs": round(read_gbs, 1),
+        "dominant_frac_of_read_stream": round(achieved / read_gbs, 4),
         "comm_bytes_per_step_per_gpu": comm_bytes,
         "e2e": e2e,
         "gpu_launches": args.steps * (d + (1 if world > 1 else 0)),
@@ -356,6 +359,28 @@ def run_ours(args) -> dict | None:
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = {k: v for k, v in cpu_reference(args.workload).items() if k != "ms_per_step"}
     return line
+
+
+def read_stream_gbs(buf) -> float:
+    """Read-only HBM bandwidth on this GPU (tv_read_stream over up to 16 GB of
+    the resident tensor, larger than L2): the ceiling of a pure streaming read."""
+    import torch
+
+    from paper_2501_03121_b200 import _lib
+
+    lib = _lib.load()
+    nbytes = min(buf.numel() * buf.element_size(), 16 << 30) & ~15
+    sink = torch.zeros(4, dtype=torch.int32, device=buf.device)
+    st = _lib.stream_ptr()
+    _lib.check(lib.tv_read_stream(buf.data_ptr(), nbytes, sink.data_ptr(), st))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        _lib.check(lib.tv_read_stream(buf.data_ptr(), nbytes, sink.data_ptr(), st))
+    e1.record()
+    torch.cuda.synchronize()
+    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
 def tv_demote_host(v, mode):
@@ -473,7 +498,13 @@ def main(argv=None) -> int:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shape", default=None, help="override the workload shape, e.g. 1024,1024,1024 (profiling)")
     args = ap.parse_args(argv)
+    if args.shape:
+        wl = dict(WORKLOADS[args.workload])
+        wl["shape"] = tuple(int(v) for v in args.shape.split(","))
+        wl["desc"] = wl["desc"].split(":")[0] + f" (shape override {args.shape})"
+        WORKLOADS[args.workload] = wl
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
 

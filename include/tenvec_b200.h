@@ -127,6 +127,12 @@ int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64
 int tv_fill(void* A, int dtype, int kind, uint64_t seed, const int64_t* ext, int d, int s,
             int64_t s_lo, int64_t s_hi, void* stream);
 
+/* Read-only streaming probe over `bytes` (16-byte aligned) of device memory:
+ * the HBM read roofline the TVC kernels are measured against in bench.py.
+ * `sink` is a device uint32 that is written only in a practically impossible
+ * case (keeps the loads from being optimised away). */
+int tv_read_stream(const void* buf, int64_t bytes, void* sink, void* stream);
+
 /* Number of SMs of the current device (grid sizing diagnostics). */
 int tv_device_sms(void);
 

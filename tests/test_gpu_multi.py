@@ -1,0 +1,102 @@
+"""One process per GPU over NCCL (RankGroup): dtvc with the split on and off the
+contraction mode, and dhopm3, against the oracle.  Needs >= 2 visible GPUs
+(skipped otherwise; run with `gpurun --gpus 2|4`)."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+def _worker(rank, world, port, q):
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    ok = []
+    try:
+        import tenvec_oracle as O
+        import paper_2501_03121_b200 as tv
+
+        group = tv.RankGroup()
+        # dtvc on a device-generated 5-mode tensor: every k, split on / off k
+        shape = (6, 8, world * 3, 5, 4)
+        full = O.fill_values(shape, "hash", seed=4).reshape(shape)
+        for name in ("f64", "f32", "bf16f32", "f16f32"):
+            mode = tv.MODES[name]
+            host = O.demote(full.reshape(-1), name).reshape(shape)
+            for s in sorted({2} | ({4} if tv.make_split_plan(4, 4, world).p_eff == world else set())):
+                dt = tv.distribute_generated(tv.Shape(shape), s, world, mode, fill="hash", seed=4, group=group)
+                parts, ranges = O.split(host, s, world)
+                for k in range(5):
+                    x = O.demote((np.arange(shape[k]) % 5) + 1.0, name).copy()
+                    res = tv.dtvc(dt, x, k)
+                    kind, outs, s2 = O.dtvc(parts, ranges, s, x, k, name)
+                    if k == s:
+                        got = res.parts[0].to_numpy()
+                        ok.append((name, s, k, bool(np.array_equal(_bits(got), _bits(outs[0].reshape(-1))))))
+                    else:
+                        got = res.parts[rank].to_numpy()
+                        ok.append((name, s, k, bool(np.array_equal(_bits(got), _bits(outs[rank].reshape(-1))))))
+        # dhopm3 over NCCL equals the in-process oracle run
+        hshape = (world * 4, 10, 9)
+        vals = np.random.default_rng(7).standard_normal(hshape)
+        for name, s in (("f64", 0), ("f64", 2), ("f32", 1), ("bf16f32", 0)):
+            mode = tv.MODES[name]
+            A = tv.Tensor.from_array(vals, mode)
+            if tv.make_split_plan(hshape[s], s, world).p_eff != world:
+                continue
+            dt = tv.distribute(A, s, world, group=group)
+            x0 = O.initial_vectors(hshape, name)
+            res = tv.dhopm3(dt, [v.copy() for v in x0], sweeps=3)
+            vecs, norms = O.dhopm3(A.to_numpy().reshape(hshape), s, world, x0, 3, name)
+            tol = {"f64": 1e-11, "f32": 1e-4, "bf16f32": 5e-2}[name]
+            same = all(np.allclose(O.promote(a, name), O.promote(b, name), rtol=tol, atol=tol)
+                       for a, b in zip(res.vectors, vecs))
+            ok.append((name, "hopm", s, bool(same and np.allclose(res.norms, norms, rtol=tol))))
+        q.put((rank, ok))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, [("error", repr(exc)[:500], 0, False)]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_rank_group_over_nccl_matches_oracle():
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(world):
+        r, res = q.get(timeout=600)
+        results[r] = res
+    for p in procs:
+        p.join(timeout=120)
+    for r, res in results.items():
+        bad = [c for c in res if not c[-1]]
+        assert not bad, (r, bad)
