@@ -77,8 +77,10 @@ int tv_tvc(const void* A, int storage, int compute, int64_t u, int64_t nk, int64
 int tv_tvc_naive(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                  const void* x, double alpha, double beta, void* y, void* stream);
 
-/* Which kernel regime tv_tvc would pick for this view (0 generic, 1 rows,
- * 2 short rows, 3 columns, 4 narrow slabs); -1 on invalid arguments. */
+/* Which kernel regime tv_tvc would pick for this view: 1 rows, 2 short rows,
+ * 3 columns, 4 narrow slabs, and their unaligned (scalar-load) forms 5 rows,
+ * 6 columns, 7 slabs, 8 small slabs staged through shared memory (0 is the
+ * naive kernel, tv_tvc_naive only); -1 on invalid arguments. */
 int tv_tvc_regime(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
 
 /* getvc over an m x n row-major view with leading dimension lda >= n.

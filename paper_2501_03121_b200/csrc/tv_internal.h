@@ -9,7 +9,17 @@
 namespace tv {
 
 // kernel regimes of tv_tvc (reported by tv_tvc_regime)
-enum { REG_GENERIC = 0, REG_ROWS = 1, REG_ROWS_SHORT = 2, REG_COLS = 3, REG_SLABS = 4 };
+enum {
+  REG_GENERIC = 0,  // the naive kernel (tv_tvc_naive only)
+  REG_ROWS = 1,
+  REG_ROWS_SHORT = 2,
+  REG_COLS = 3,
+  REG_SLABS = 4,
+  REG_ROWS_U = 5,  // unaligned forms: scalar, lane-interleaved loads
+  REG_COLS_U = 6,
+  REG_SLABS_U = 7,
+  REG_STAGED = 8  // small slabs staged through shared memory (cp.async)
+};
 
 // the five valid (storage, compute) pairs of precision.py:81-87
 enum { MODE_INVALID = -1, MODE_F64 = 0, MODE_F32 = 1, MODE_F32F64 = 2, MODE_F16F32 = 3, MODE_BF16F32 = 4 };

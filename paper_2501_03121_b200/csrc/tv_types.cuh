@@ -95,6 +95,25 @@ __device__ __forceinline__ uint4 ld_stream16(const void* p) {
   return r;
 }
 
+// one streamed element (lane-interleaved scalar loads of unaligned views).
+// volatile keeps a batch of these in issue order: without it the compiler
+// sinks each load next to its FMA and only one load per lane is in flight.
+__device__ __forceinline__ double ld_stream_elem(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_stream_elem(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint16_t ld_stream_elem(const uint16_t* p) {
+  uint16_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+
 template <int SD>
 union Pack16 {
   uint4 u;

@@ -6,32 +6,39 @@
 // ever needs an unfolding copy and every tensor byte is streamed from HBM
 // exactly once.  The reference runs one BLAS matvec for k = d-1 and a Python
 // loop of u BLAS vecmats otherwise; here one launch covers the whole view and
-// the host picks one of five regimes from the view's shape:
+// the host picks a regime from the view's shape and alignment:
 //
-//   ROWS       v == 1, rows of >= 8 16-byte vectors: G lanes per row (G in
-//              {4,8,16,32}, chosen to minimise idle lanes), 128-bit loads,
-//              x promoted once into shared memory, xor-shuffle row reduction.
-//   ROWS_SHORT v == 1, rows of 1..7 vectors: lanes tile whole rows
-//              (R = 32 / nkv rows per warp step), a segmented in-order
-//              shuffle sum per row.
-//   COLS       v >= 32 vectors: a CTA owns a 512-byte column stripe of one
-//              slab; its 8 warps split the n_k rows round-robin, accumulate in
-//              registers, and a fixed-order shared-memory reduction finishes.
-//   SLABS      1 < v < 32 vectors: one warp streams a whole slab; R = 32 / vv
-//              rows per step so every warp load is one contiguous run, then a
-//              fixed-order cross-row reduction in shared memory.
-//   GENERIC    anything not 16-byte aligned: scalar loads, same math.
+//   ROWS        v == 1: G lanes per row (G chosen so each lane keeps UNR loads
+//               in flight with few idle slots), x promoted once into shared
+//               memory, xor-shuffle row reduction.
+//   ROWS_SHORT  v == 1, aligned rows of 1..7 16-byte vectors: lanes tile whole
+//               rows (R = 32 / nkv rows per warp step), in-order segmented
+//               shuffle sum per row.
+//   COLS        v >= 32 units: a CTA = CW 32-lane column stripes x JR row
+//               phases of one slab (JR from n_k: 1 for short columns -- no
+//               reduction -- up to 8 for long ones), registers accumulate, a
+//               fixed-order shared-memory fold finishes when JR > 1.
+//   SLABS       1 < v < 32 units: one warp per slab, R = 32 / units rows per
+//               step so each warp load is one contiguous run, then a
+//               fixed-order fold across rows in shared memory.
+//
+// Every regime has an aligned form (one 16-byte ld.global.nc.L1::no_allocate
+// per lane, "unit" = 16 bytes) and an unaligned form for rows or slabs that do
+// not start on 16 bytes (odd extents such as the paper's 979^3 or 13^8 in
+// fp64): scalar loads interleaved so consecutive lanes read consecutive
+// elements ("unit" = one element; COLS lanes own VEC columns 32 apart).
 //
 // All regimes accumulate in the compute type, apply alpha after the dot
 // product and beta * y after that (kernels.py:113-118), and demote once on
 // store.  beta == 0 never reads y.  The reduction order of every output element
-// depends only on (u, n_k, v, dtype): reruns and ranks reproduce bits.
-// There are no tensor cores here: the arithmetic intensity is 0.25-1 FLOP/B.
+// depends only on (u, n_k, v, strides, dtype): reruns and ranks reproduce
+// bits.  There are no tensor cores here: arithmetic intensity is 0.25-1 FLOP/B.
 
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "tv_internal.h"
 #include "tv_types.cuh"
@@ -39,16 +46,42 @@
 namespace tv {
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// a lane's load: one 16-byte vector (AL) or one element
+template <int SD, typename C, bool AL>
+struct Unit {
+  using T = typename St<SD>::T;
+  static constexpr int N = AL ? VecN<SD>::N : 1;
+  using Raw = typename std::conditional<AL, uint4, T>::type;
+  static __device__ __forceinline__ Raw load(const T* p) {
+    if constexpr (AL) return ld_stream16(p);
+    else return ld_stream_elem(p);
+  }
+  static __device__ __forceinline__ void widen(const Raw& r, C (&out)[N]) {
+    if constexpr (AL) unpack<SD, C>(r, out);
+    else out[0] = promote<SD, C>(r);
+  }
+};
 
 // ---------------------------------------------------------------- ROWS ----
-template <int SD, typename C, int G, int UNR, bool XS>
+// Row `row` starts at A + row * su.  Its body is read as 16-byte vectors
+// q = g, g + G, ... (G lanes per row); with PEEL the row may start anywhere
+// (odd extents such as 979 or 175 in fp64): the elements before its first
+// 16-byte boundary (head) and after its last full vector (tail) are folded by
+// scalar loads, so the body still streams as full vectors.
+// Every lane issues QB loads per batch (one memory round trip): a batch walks
+// QB vectors of one row (RS = 1, long rows) or QB / RS vectors of each of RS
+// row steps (short rows).
+template <int SD, typename C, int G, int RS, int QB, bool XS, bool PEEL>
 __global__ void __launch_bounds__(kThreads)
     k_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
-           typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, C alpha, C beta,
+           typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t su, C alpha, C beta,
            int has_beta) {
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
-  constexpr int RPW = 32 / G;  // rows per warp step
+  constexpr int QPL = QB / RS;  // loads per lane per row in one batch
+  constexpr int RPW = 32 / G;   // rows per warp step
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* xs = reinterpret_cast<C*>(smem_raw);
   if (XS) {
@@ -58,54 +91,110 @@ __global__ void __launch_bounds__(kThreads)
   const int lane = threadIdx.x & 31;
   const int g = lane % G;
   const int rs = lane / G;
-  const int64_t nkv = nk / VEC;
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  for (int64_t row0 = gw * RPW; row0 < u; row0 += warps_total * RPW) {
-    const int64_t row = row0 + rs;
-    C acc[VEC];
+  const int64_t warps_total = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  auto xv = [&](int64_t j) -> C { return XS ? xs[j] : promote<SD, C>(__ldg(x + j)); };
+  // head length (elements before the first 16-byte boundary) of a row
+  auto head_of = [&](const T* rp) -> int64_t {
+    if constexpr (!PEEL) return 0;
+    const int64_t h = (int64_t)(((16u - (unsigned)(reinterpret_cast<uintptr_t>(rp) & 15u)) & 15u) / sizeof(T));
+    return h < nk ? h : nk;
+  };
+  auto fold_vec = [&](const uint4& raw, int64_t j0, C (&acc)[VEC]) {
+    C a[VEC];
+    unpack<SD, C>(raw, a);
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) acc[e] = C(0);
-    if (row < u) {
-      const uint4* rp = reinterpret_cast<const uint4*>(A + row * nk);
-      for (int64_t q0 = g; q0 < nkv; q0 += (int64_t)G * UNR) {
-        uint4 buf[UNR];
+    for (int e = 0; e < VEC; ++e) acc[e] = fma(a[e], xv(j0 + e), acc[e]);
+  };
+  // head and tail elements of a peeled row (returned, added to acc[0] after)
+  auto fold_edges = [&](const T* rp, int64_t h, int64_t nb) -> C {
+    C e = C(0);
+    if constexpr (PEEL) {
+      for (int64_t j = g; j < h; j += G) e = fma(promote<SD, C>(__ldg(rp + j)), xv(j), e);
+      for (int64_t j = h + nb * VEC + g; j < nk; j += G) e = fma(promote<SD, C>(__ldg(rp + j)), xv(j), e);
+    }
+    return e;
+  };
+  for (int64_t row0 = gw * RPW * RS; row0 < u; row0 += warps_total * RPW * RS) {
+    C acc[RS][VEC];
 #pragma unroll
-        for (int t = 0; t < UNR; ++t) {
-          const int64_t q = q0 + (int64_t)t * G;
-          if (q < nkv) buf[t] = ld_stream16(rp + q);
+    for (int r2 = 0; r2 < RS; ++r2)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[r2][e] = C(0);
+    if constexpr (RS == 1) {
+      const int64_t row = row0 + rs;
+      if (row < u) {
+        const T* rp = A + row * su;
+        const int64_t h = head_of(rp);
+        const int64_t nb = (nk - h) / VEC;
+        const uint4* body = reinterpret_cast<const uint4*>(rp + h);
+        // full batches without predicates, so all QPL loads issue back to back
+        int64_t q0 = g;
+        for (; q0 + (int64_t)(QPL - 1) * G < nb; q0 += (int64_t)G * QPL) {
+          uint4 buf[QPL];
+#pragma unroll
+          for (int t = 0; t < QPL; ++t) buf[t] = ld_stream16(body + q0 + (int64_t)t * G);
+#pragma unroll
+          for (int t = 0; t < QPL; ++t) fold_vec(buf[t], h + (q0 + (int64_t)t * G) * VEC, acc[0]);
         }
+        for (; q0 < nb; q0 += G) fold_vec(ld_stream16(body + q0), h + q0 * VEC, acc[0]);
+        if constexpr (PEEL) acc[0][0] += fold_edges(rp, h, nb);
+      }
+    } else {
+      // loads of idle lanes / rows past the end are clamped to an in-range
+      // vector (and not folded) so the batch issues without predicates
+      uint4 buf[RS][QPL];
 #pragma unroll
-        for (int t = 0; t < UNR; ++t) {
-          const int64_t q = q0 + (int64_t)t * G;
-          if (q < nkv) {
-            C a[VEC];
-            unpack<SD, C>(buf[t], a);
+      for (int r2 = 0; r2 < RS; ++r2) {
+        const int64_t row = row0 + (int64_t)r2 * RPW + rs;
+        const T* rp = A + (row < u ? row : u - 1) * su;
+        const int64_t h = head_of(rp);
+        const int64_t nb = (nk - h) / VEC;
+        const uint4* body = reinterpret_cast<const uint4*>(rp + h);
+        if (!PEEL || nb > 0) {
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-              const C xv = XS ? xs[q * VEC + e] : promote<SD, C>(__ldg(x + q * VEC + e));
-              acc[e] = fma(a[e], xv, acc[e]);
-            }
+          for (int t = 0; t < QPL; ++t) {
+            const int64_t q = g + (int64_t)t * G;
+            buf[r2][t] = ld_stream16(body + (q < nb ? q : nb - 1));
           }
         }
       }
+#pragma unroll
+      for (int r2 = 0; r2 < RS; ++r2) {
+        const int64_t row = row0 + (int64_t)r2 * RPW + rs;
+        if (row < u) {
+          const T* rp = A + row * su;
+          const int64_t h = head_of(rp);
+          const int64_t nb = (nk - h) / VEC;
+#pragma unroll
+          for (int t = 0; t < QPL; ++t) {
+            const int64_t q = g + (int64_t)t * G;
+            if (q < nb) fold_vec(buf[r2][t], h + q * VEC, acc[r2]);
+          }
+          if constexpr (PEEL) acc[r2][0] += fold_edges(rp, h, nb);
+        }
+      }
     }
-    C s = acc[0];
 #pragma unroll
-    for (int e = 1; e < VEC; ++e) s += acc[e];
+    for (int r2 = 0; r2 < RS; ++r2) {
+      const int64_t row = row0 + (int64_t)r2 * RPW + rs;
+      C s = acc[r2][0];
 #pragma unroll
-    for (int off = G / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (g == 0 && row < u) y[row] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + row);
+      for (int e = 1; e < VEC; ++e) s += acc[r2][e];
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (g == 0 && row < u) y[row] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + row);
+    }
   }
 }
 
 // ---------------------------------------------------------- ROWS_SHORT ----
-// rows of nkv in [1, 7] vectors; lanes (r = lane / nkv, c = lane % nkv)
+// aligned rows of nkv in [1, 7] vectors; lanes (r = lane / nkv, c = lane % nkv)
 template <int SD, typename C, int UNR>
 __global__ void __launch_bounds__(kThreads)
     k_rows_short(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
-                 typename St<SD>::T* __restrict__ y, int64_t u, int nk, C alpha, C beta,
-                 int has_beta) {
+                 typename St<SD>::T* __restrict__ y, int64_t u, int nk, int64_t su, C alpha,
+                 C beta, int has_beta) {
   constexpr int VEC = VecN<SD>::N;
   __shared__ C xs[8 * VEC];
   const int nkv = nk / VEC;
@@ -116,15 +205,15 @@ __global__ void __launch_bounds__(kThreads)
   const int r = lane / nkv;
   const int c = lane - r * nkv;
   const bool active = r < R;
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t warps_total = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int64_t step = (int64_t)R * UNR;
   for (int64_t row0 = gw * step; row0 < u; row0 += warps_total * step) {
     uint4 buf[UNR];
 #pragma unroll
     for (int t = 0; t < UNR; ++t) {
       const int64_t row = row0 + (int64_t)t * R + r;
-      if (active && row < u) buf[t] = ld_stream16(A + row * nk + c * VEC);
+      if (active && row < u) buf[t] = ld_stream16(A + row * su + c * VEC);
     }
 #pragma unroll
     for (int t = 0; t < UNR; ++t) {
@@ -138,10 +227,7 @@ __global__ void __launch_bounds__(kThreads)
       }
       // in-order segmented sum over the nkv lanes of a row: ((p0 + p1) + p2) ...
       C s = p;
-      for (int i = 1; i < nkv; ++i) {
-        const C o = __shfl_down_sync(0xffffffffu, p, i);
-        s += o;
-      }
+      for (int i = 1; i < nkv; ++i) s += __shfl_down_sync(0xffffffffu, p, i);
       if (active && c == 0 && row < u)
         y[row] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + row);
     }
@@ -149,115 +235,167 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- COLS ----
-// CTA = 8 warps over a 32-vector column stripe of slab i; warp w sums rows
-// j = w, w + 8, ...; smem reduction over w in ascending order.
-template <int SD, typename C, int UNR>
+// slab i at A + i * su, row j at + j * sk.  Warp (stripe, r) of the CTA sums
+// rows j = r, r + JR, ... of its stripe.  Aligned: lane owns one 16-byte
+// vector (VEC adjacent columns); unaligned: lane owns VEC columns 32 apart, so
+// each of its scalar loads is part of one contiguous 32-element warp access.
+template <int SD, typename C, int JR, int UNR, bool AL>
 __global__ void __launch_bounds__(kThreads)
     k_cols(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
-           typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t v, int64_t ntile,
-           C alpha, C beta, int has_beta) {
+           typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t v, int64_t su,
+           int64_t sk, int64_t ntile, C alpha, C beta, int has_beta) {
+  using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
-  constexpr int JR = kThreads / 32;
-  __shared__ C red[JR][32][VEC + (sizeof(C) == 8 ? 0 : 1)];
+  constexpr int CW = kWarps / JR;
+  __shared__ C red[JR > 1 ? JR : 1][CW][32][VEC + (sizeof(C) == 8 ? 0 : 1)];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const int64_t vv = v / VEC;
+  const int stripe = w % CW;
+  const int r = w / CW;
   const int64_t i = blockIdx.x / ntile;
   const int64_t tile = blockIdx.x - i * ntile;
-  const int64_t col = tile * 32 + lane;
-  const bool active = col < vv;
-  const auto* base = A + i * nk * v + col * VEC;
+  const int64_t sbase = (tile * CW + stripe) * 32;  // first unit of this warp's stripe
+  // column of accumulator e
+  auto col_of = [&](int e) -> int64_t {
+    return AL ? (sbase + lane) * VEC + e : sbase * VEC + (int64_t)e * 32 + lane;
+  };
+  const bool any = AL ? (sbase + lane) * VEC < v : sbase * VEC + lane < v;
+  const T* base = A + i * su;
   C acc[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc[e] = C(0);
-  for (int64_t j0 = w; j0 < nk; j0 += (int64_t)JR * UNR) {
-    uint4 buf[UNR];
-#pragma unroll
-    for (int t = 0; t < UNR; ++t) {
-      const int64_t j = j0 + (int64_t)t * JR;
-      if (active && j < nk) buf[t] = ld_stream16(base + j * v);
-    }
-#pragma unroll
-    for (int t = 0; t < UNR; ++t) {
-      const int64_t j = j0 + (int64_t)t * JR;
-      if (active && j < nk) {
+  if (any) {
+    // full batches of UNR rows without predicates (all loads issue back to
+    // back), then the remaining rows one at a time
+    int64_t j0 = r;
+    if constexpr (AL) {
+      const T* cb = base + (sbase + lane) * VEC;
+      auto fold = [&](const uint4& raw, int64_t j) {
         const C xj = promote<SD, C>(__ldg(x + j));
         C a[VEC];
-        unpack<SD, C>(buf[t], a);
+        unpack<SD, C>(raw, a);
 #pragma unroll
         for (int e = 0; e < VEC; ++e) acc[e] = fma(a[e], xj, acc[e]);
+      };
+      for (; j0 + (int64_t)(UNR - 1) * JR < nk; j0 += (int64_t)JR * UNR) {
+        uint4 buf[UNR];
+#pragma unroll
+        for (int t = 0; t < UNR; ++t) buf[t] = ld_stream16(cb + (j0 + (int64_t)t * JR) * sk);
+#pragma unroll
+        for (int t = 0; t < UNR; ++t) fold(buf[t], j0 + (int64_t)t * JR);
+      }
+      for (; j0 < nk; j0 += JR) fold(ld_stream16(cb + j0 * sk), j0);
+    } else {
+      // predicated batches (measured faster for scalar columns than split loops)
+      bool ok[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) ok[e] = col_of(e) < v;
+      for (; j0 < nk; j0 += (int64_t)JR * UNR) {
+        T buf[UNR][VEC];
+#pragma unroll
+        for (int t = 0; t < UNR; ++t) {
+          const int64_t j = j0 + (int64_t)t * JR;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            if (j < nk && ok[e]) buf[t][e] = ld_stream_elem(base + j * sk + col_of(e));
+        }
+#pragma unroll
+        for (int t = 0; t < UNR; ++t) {
+          const int64_t j = j0 + (int64_t)t * JR;
+          if (j < nk) {
+            const C xj = promote<SD, C>(__ldg(x + j));
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+              if (ok[e]) acc[e] = fma(promote<SD, C>(buf[t][e]), xj, acc[e]);
+          }
+        }
       }
     }
   }
-#pragma unroll
-  for (int e = 0; e < VEC; ++e) red[w][lane][e] = acc[e];
-  __syncthreads();
-  if (w == 0 && active) {
-    const int64_t jr = nk < JR ? nk : JR;
+  if constexpr (JR == 1) {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      C s = red[0][lane][e];
-      for (int k = 1; k < jr; ++k) s += red[k][lane][e];
-      const int64_t o = i * v + col * VEC + e;
-      y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+      const int64_t c = col_of(e);
+      if (c < v) {
+        const int64_t o = i * v + c;
+        y[o] = epilogue<SD, C>(acc[e], alpha, beta, has_beta != 0, y + o);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) red[r][stripe][lane][e] = acc[e];
+    __syncthreads();
+    if (r == 0) {
+      const int64_t jr = nk < JR ? nk : JR;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const int64_t c = col_of(e);
+        if (c < v) {
+          C s = red[0][stripe][lane][e];
+          for (int k = 1; k < jr; ++k) s += red[k][stripe][lane][e];
+          const int64_t o = i * v + c;
+          y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+        }
+      }
     }
   }
 }
 
 // --------------------------------------------------------------- SLABS ----
-// one warp per slab of nk x v with vv = v / VEC in [1, 31] vectors per row;
-// lanes (r = lane / vv, c = lane % vv), R = 32 / vv rows per step.
-template <int SD, typename C, int UNR>
+// one warp per slab; `units` = v / VEC (aligned) or v (unaligned) in [1, 31];
+// lanes (r = lane / units, c = lane % units), R = 32 / units rows per step.
+template <int SD, typename C, int UNR, bool AL>
 __global__ void __launch_bounds__(kThreads)
     k_slabs(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
-            typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int v, C alpha, C beta,
-            int has_beta) {
-  constexpr int VEC = VecN<SD>::N;
-  constexpr int NW = kThreads / 32;
-  __shared__ C red[NW][32][VEC + (sizeof(C) == 8 ? 0 : 1)];
+            typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int v, int64_t su,
+            int64_t sk, C alpha, C beta, int has_beta) {
+  using U = Unit<SD, C, AL>;
+  constexpr int N = U::N;
+  __shared__ C red[kWarps][32][N + (sizeof(C) == 8 ? 0 : 1)];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const int vv = v / VEC;
-  const int R = 32 / vv;
-  const int r = lane / vv;
-  const int c = lane - r * vv;
+  const int units = v / N;
+  const int R = 32 / units;
+  const int r = lane / units;
+  const int c = lane - r * units;
   const bool active = r < R;
-  const int64_t warps_total = (int64_t)gridDim.x * NW;
-  const int64_t gw = (int64_t)blockIdx.x * NW + w;
+  const int64_t warps_total = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + w;
   for (int64_t i = gw; i < u; i += warps_total) {
-    const auto* base = A + i * nk * v + c * VEC;
-    C acc[VEC];
+    const auto* base = A + i * su + c * N;
+    C acc[N];
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) acc[e] = C(0);
+    for (int e = 0; e < N; ++e) acc[e] = C(0);
+    // predicated batches (measured faster here than split full/remainder loops)
     for (int64_t j0 = r; j0 < nk; j0 += (int64_t)R * UNR) {
-      uint4 buf[UNR];
+      typename U::Raw buf[UNR];
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
         const int64_t j = j0 + (int64_t)t * R;
-        if (active && j < nk) buf[t] = ld_stream16(base + j * v);
+        if (active && j < nk) buf[t] = U::load(base + j * sk);
       }
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
         const int64_t j = j0 + (int64_t)t * R;
         if (active && j < nk) {
           const C xj = promote<SD, C>(__ldg(x + j));
-          C a[VEC];
-          unpack<SD, C>(buf[t], a);
+          C a[N];
+          U::widen(buf[t], a);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[e] = fma(a[e], xj, acc[e]);
+          for (int e = 0; e < N; ++e) acc[e] = fma(a[e], xj, acc[e]);
         }
       }
     }
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) red[w][lane][e] = acc[e];
+    for (int e = 0; e < N; ++e) red[w][lane][e] = acc[e];
     __syncwarp();
-    if (lane < vv) {
+    if (lane < units) {
       const int64_t rr = nk < R ? nk : R;
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) {
+      for (int e = 0; e < N; ++e) {
         C s = red[w][lane][e];
-        for (int k = 1; k < rr; ++k) s += red[w][lane + k * vv][e];
-        const int64_t o = i * v + (int64_t)lane * VEC + e;
+        for (int k = 1; k < rr; ++k) s += red[w][lane + k * units][e];
+        const int64_t o = i * v + (int64_t)lane * N + e;
         y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
       }
     }
@@ -265,18 +403,148 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// ------------------------------------------------------------- GENERIC ----
-// element (i, j, l) at A[i * su + j * sk + l]; used for unaligned views and the
-// strided getvc.  v == 1: one warp per row, lanes stride the row (coalesced).
+// -------------------------------------------------------------- STAGED ----
+// Small slabs (<= kStageBytes / 2), aligned or not: whole-slab tiles of the
+// flat buffer are copied global -> shared with 16-byte cp.async (aligned-down
+// start, zero-filled ragged end), double-buffered per CTA, so HBM sees pure
+// contiguous 512-byte-per-warp streaming whatever n_k and v are; the dot
+// products are then read from shared memory.  Output o of a tile = (slab
+// o / v, column o % v); G lanes share an output (j = g, g + G, ...) and
+// combine with an xor shuffle.  For v == 1, G lanes read consecutive words.
+constexpr int kStageBytes = 16384;
+constexpr int kStagedRowBytes = 512;  // v == 1 rows up to this size are staged
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int SD, typename C, bool VROW>
+__global__ void __launch_bounds__(kThreads)
+    k_staged(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+             typename St<SD>::T* __restrict__ y, int64_t u, int nk, int v, int spt, int64_t ntiles,
+             int G, C alpha, C beta, int has_beta) {
+  using T = typename St<SD>::T;
+  constexpr int SB = sizeof(T);
+  constexpr int VEC = VecN<SD>::N;
+  constexpr int NA = VROW ? VEC : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int xs_pad = (nk * (int)sizeof(C) + 15) / 16 * 16;
+  C* xs = reinterpret_cast<C*>(smem_raw);
+  unsigned char* const stage0 = smem_raw + xs_pad;
+  auto stage = [&](int k) { return stage0 + (k & 1) * (kStageBytes + 16); };
+  C* red = reinterpret_cast<C*>(smem_raw + xs_pad + 2 * (kStageBytes + 16));
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) xs[i] = promote<SD, C>(x[i]);
+
+  const int L = nk * v;
+  const uintptr_t gbase = reinterpret_cast<uintptr_t>(A);
+  const int64_t total_bytes = u * (int64_t)L * SB;
+  auto issue = [&](int64_t tile, unsigned char* dst) {
+    const int64_t b0 = tile * spt * (int64_t)L * SB;
+    const int64_t s1 = (tile + 1) * spt < u ? (tile + 1) * spt : u;
+    const int64_t a0 = b0 & ~(int64_t)15;
+    const int nvec = (int)((s1 * (int64_t)L * SB - a0 + 15) / 16);
+    for (int vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
+      const int64_t off = a0 + (int64_t)vi * 16;
+      const int64_t left = total_bytes - off;
+      cp_async16(dst + vi * 16, reinterpret_cast<const void*>(gbase + off), left >= 16 ? 16 : (int)left);
+    }
+    cp_async_commit();
+  };
+
+  // thread = (gi, oi): output oi of each pass of `per` outputs, j-slice gi of G
+  const int per = kThreads / G;
+  const int gi = threadIdx.x / per;
+  const int oi = threadIdx.x - gi * per;
+  // units of a "row" (output's j range): 16-byte chunks when VROW, else elements
+  const int nunits = VROW ? nk / VEC : nk;
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, stage(0));
+  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+    const int64_t next = tile + gridDim.x;
+    if (next < ntiles) {
+      issue(next, stage(it + 1));
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int64_t s0 = tile * spt;
+    const int ns = (int)(spt < u - s0 ? spt : u - s0);
+    const T* t = reinterpret_cast<const T*>(stage(it) + ((s0 * (int64_t)L * SB) & 15));
+    const int outs = ns * v;
+    for (int ob = 0; ob < outs; ob += per) {  // block-uniform trip count
+      const int o = ob + oi;
+      C acc[NA];
+#pragma unroll
+      for (int e = 0; e < NA; ++e) acc[e] = C(0);
+      if (o < outs) {
+        const int s = o / v;
+        const int l = o - s * v;
+        if constexpr (VROW) {
+          // v == 1, 16-byte rows: rotate the start chunk by the row index when
+          // the row has an even chunk count so a quarter-warp hits 8 banks
+          const uint4* rp = reinterpret_cast<const uint4*>(t + s * nk);
+          const int rot = (nunits & 1) ? 0 : s;
+          for (int i = gi; i < nunits; i += G) {
+            int q = i + rot % nunits;
+            q = q >= nunits ? q - nunits : q;
+            C a[VEC];
+            unpack<SD, C>(rp[q], a);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[e] = fma(a[e], xs[q * VEC + e], acc[e]);
+          }
+        } else if (v == 1) {
+          const T* rp = t + s * nk;
+          const int rot = (nk & 1) ? 0 : s % nk;
+          for (int i = gi; i < nk; i += G) {
+            int j = i + rot;
+            j = j >= nk ? j - nk : j;
+            acc[0] = fma(promote<SD, C>(rp[j]), xs[j], acc[0]);
+          }
+        } else {
+          const T* sp = t + s * L + l;
+          for (int j = gi; j < nk; j += G) acc[0] = fma(promote<SD, C>(sp[j * v]), xs[j], acc[0]);
+        }
+      }
+      C sum = acc[0];
+#pragma unroll
+      for (int e = 1; e < NA; ++e) sum += acc[e];
+      if (G > 1) {
+        red[threadIdx.x] = sum;
+        __syncthreads();
+        if (gi == 0 && o < outs) {
+          for (int k = 1; k < G; ++k) sum += red[k * per + oi];
+          const int64_t oy = s0 * v + o;
+          y[oy] = epilogue<SD, C>(sum, alpha, beta, has_beta != 0, y + oy);
+        }
+        __syncthreads();
+      } else if (o < outs) {
+        const int64_t oy = s0 * v + o;
+        y[oy] = epilogue<SD, C>(sum, alpha, beta, has_beta != 0, y + oy);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------- NAIVE ----
+// the "looped" cross-check (tv_tvc_naive): plain scalar loops, element
+// (i, j, l) at A[i * su + j * sk + l].  v == 1: one warp per row.
 template <int SD, typename C>
 __global__ void __launch_bounds__(kThreads)
-    k_generic_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
-                   typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t su,
-                   int64_t sk, C alpha, C beta, int has_beta) {
+    k_naive_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+                 typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t su, int64_t sk,
+                 C alpha, C beta, int has_beta) {
   const int lane = threadIdx.x & 31;
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < u;
-       i += warps_total) {
+  const int64_t warps_total = (int64_t)gridDim.x * kWarps;
+  for (int64_t i = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); i < u; i += warps_total) {
     C s = C(0);
     for (int64_t j = lane; j < nk; j += 32)
       s = fma(promote<SD, C>(A[i * su + j * sk]), promote<SD, C>(x[j]), s);
@@ -288,9 +556,9 @@ __global__ void __launch_bounds__(kThreads)
 
 template <int SD, typename C>
 __global__ void __launch_bounds__(kThreads)
-    k_generic_cols(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
-                   typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t v,
-                   int64_t su, int64_t sk, C alpha, C beta, int has_beta) {
+    k_naive_cols(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+                 typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t v, int64_t su,
+                 int64_t sk, C alpha, C beta, int has_beta) {
   const int64_t total = u * v;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
        o += (int64_t)gridDim.x * blockDim.x) {
@@ -325,129 +593,276 @@ static unsigned grid_for(int64_t work_items, int64_t per_block, int waves_cap) {
   return (unsigned)need;
 }
 
-// pick G in {32, 16, 8, 4}: the widest group idling at most 1/8 of the
-// vector slots of a row, else the one idling the fewest
-static int pick_row_group(int64_t nkv) {
+static int64_t waste_of(int64_t n, int G) { return cdiv(n, G) * G - n; }
+
+// Lanes per row.  A warp load instruction costs one L1 wavefront per 128-byte
+// line it touches, so a row's lanes must cover >= 128 contiguous bytes per
+// instruction (G * unit_bytes >= 128): short rows take G = pow2ceil(units)
+// (idle lanes, but adjacent rows stay contiguous); long rows the widest
+// G >= gmin idling at most 1/8 of the unit slots, else the fewest.
+static int pick_row_group(int64_t nunits, int unit_bytes) {
+  if (nunits <= 32) {
+    int G = 1;
+    while (G < nunits) G <<= 1;
+    return G;
+  }
+  const int gmin = std::max(1, std::min(32, 128 / unit_bytes));
   int best = 32;
-  int64_t best_waste = -1;
-  for (int G : {32, 16, 8, 4}) {
-    const int64_t waste = cdiv(nkv, G) * G - nkv;
-    if (waste * 8 <= nkv) return G;
-    if (best_waste < 0 || waste < best_waste) {
-      best = G;
-      best_waste = waste;
-    }
+  for (int G : {32, 16, 8, 4, 2, 1}) {
+    if (G < gmin) break;
+    if (waste_of(nunits, G) * 8 <= nunits) return G;
+    if (waste_of(nunits, G) < waste_of(nunits, best)) best = G;
   }
   return best;
+}
+
+// row steps per batch so a lane keeps QB loads in flight on short rows
+static int pick_row_steps(int64_t nunits, int G, int qb) {
+  const int64_t qpl = cdiv(nunits, G);
+  if (qpl * 4 <= qb) return 4;
+  if (qpl * 2 <= qb) return 2;
+  return 1;
+}
+
+// row phases of the COLS kernel: enough rows per warp for deep load
+// pipelines, as many 32-lane stripes per CTA as the slab is wide, and at
+// least 4 CTAs per SM so small views still fill the GPU
+static int pick_col_phases(int64_t nk, int64_t stripes, int64_t u) {
+  int jr = nk >= 1024 ? 8 : nk >= 512 ? 4 : nk >= 256 ? 2 : 1;
+  int cw_max = 1;
+  while (cw_max < kWarps && cw_max * 2 <= stripes) cw_max *= 2;
+  if (kWarps / jr > cw_max) jr = kWarps / cw_max;
+  const int64_t want = 4LL * sm_count();
+  while (jr < kWarps && jr < nk && u * cdiv(stripes, kWarps / jr) < want) jr *= 2;
+  return jr;
+}
+
+static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t v, int64_t su,
+                          int64_t sk) {
+  const int VEC = 16 / sb;
+  const bool base_al = (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  const bool su_al = u <= 1 || (su * sb) % 16 == 0;
+  const bool contiguous = su == nk * v && sk == v;
+  const bool al_rows = base_al && su_al && nk % VEC == 0;
+  const bool al_cols = base_al && su_al && (sk * sb) % 16 == 0 && v % VEC == 0;
+  const bool stageable = base_al && contiguous && u > 1 && nk * v * sb <= kStageBytes;
+  // TENVEC_B200_FORCE=<regime number> pins a regime wherever it is valid
+  // (kernel A/B measurements); anything else falls through to the heuristics
+  static const int forced = [] {
+    const char* e = getenv("TENVEC_B200_FORCE");
+    return e ? atoi(e) : -1;
+  }();
+  if (forced > 0) {
+    const bool ok = (forced == REG_ROWS && v == 1 && al_rows) ||
+                    (forced == REG_ROWS_SHORT && v == 1 && al_rows && nk / VEC <= 8) ||
+                    (forced == REG_ROWS_U && v == 1) || (forced == REG_COLS && v > 1 && al_cols) ||
+                    (forced == REG_SLABS && v > 1 && al_cols && v / VEC < 32) ||
+                    (forced == REG_COLS_U && v > 1) || (forced == REG_SLABS_U && v > 1 && v < 32) ||
+                    (forced == REG_STAGED && stageable);
+    if (ok) return forced;
+  }
+  // measured on B200 (profiles/r01_regime_ab.txt): aligned views always stream
+  // best straight from HBM -- rows of any length through ROWS (G lanes per
+  // row, batched row steps), wide slabs through COLS, narrow ones through
+  // SLABS.  Views whose rows/slabs are NOT 16-byte multiples and small enough
+  // go through STAGED (contiguous cp.async tiles), which beats scalar loads
+  // 2-4x there; larger unaligned views use the peeled / scalar forms.
+  if (v == 1) {
+    if (al_rows) return REG_ROWS;
+    if (stageable && nk * sb <= kStagedRowBytes) return REG_STAGED;
+    return REG_ROWS_U;
+  }
+  if (al_cols) return (v / VEC >= 32) ? REG_COLS : REG_SLABS;
+  if (stageable && nk * v * sb <= kStageBytes / 2) return REG_STAGED;
+  return v >= 32 ? REG_COLS_U : REG_SLABS_U;
 }
 
 int regime_of(const void* A, int storage, int64_t u, int64_t nk, int64_t v) {
   if (u < 0 || nk < 1 || v < 1) return -1;
   const int sb = dtype_bytes(storage);
   if (sb <= 0) return -1;
-  const int VEC = 16 / sb;
-  const bool aligned = (reinterpret_cast<uintptr_t>(A) & 15) == 0;
-  if (v == 1) {
-    if (!aligned || nk % VEC != 0) return REG_GENERIC;
-    return (nk / VEC >= 8) ? REG_ROWS : REG_ROWS_SHORT;
-  }
-  if (!aligned || v % VEC != 0) return REG_GENERIC;
-  return (v / VEC >= 32) ? REG_COLS : REG_SLABS;
+  return regime_strided(A, sb, u, nk, v, nk * v, v);
 }
 
-template <int SD, typename C, int G>
-static void launch_rows(const void* A, const void* x, void* y, int64_t u, int64_t nk, C al, C be,
-                        int hb, cudaStream_t st) {
+constexpr int kRowBatch = 4;  // 16-byte loads per lane per batch
+
+template <int SD, typename C, int G, int RS, bool PEEL>
+static void launch_rows(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t su,
+                        C al, C be, int hb, cudaStream_t st) {
   using T = typename St<SD>::T;
-  constexpr int UNR = 4;
   const size_t xs_bytes = (size_t)nk * sizeof(C);
-  const int64_t rows_per_block = (kThreads / 32) * (32 / G);
+  const int64_t rows_per_block = (int64_t)kWarps * (32 / G) * RS;
   const unsigned grid = grid_for(u, rows_per_block, 32);
   if (xs_bytes <= 96 * 1024) {
-    auto kern = k_rows<SD, C, G, UNR, true>;
+    auto kern = k_rows<SD, C, G, RS, kRowBatch, true, PEEL>;
     if (xs_bytes > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs_bytes);
-    kern<<<grid, kThreads, xs_bytes, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, al, be, hb);
-  } else {
-    k_rows<SD, C, G, UNR, false>
-        <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, al, be, hb);
+    kern<<<grid, kThreads, xs_bytes, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
+  } else if constexpr (G == 32 && RS == 1) {
+    // rows longer than the shared-memory copy of x: x through L1
+    k_rows<SD, C, 32, 1, kRowBatch, false, PEEL>
+        <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
   }
+}
+
+template <int SD, typename C, int G, bool PEEL>
+static void rows_by_steps(int RS, const void* A, const void* x, void* y, int64_t u, int64_t nk,
+                          int64_t su, C al, C be, int hb, cudaStream_t st) {
+  if (RS == 4) launch_rows<SD, C, G, 4, PEEL>(A, x, y, u, nk, su, al, be, hb, st);
+  else if (RS == 2) launch_rows<SD, C, G, 2, PEEL>(A, x, y, u, nk, su, al, be, hb, st);
+  else launch_rows<SD, C, G, 1, PEEL>(A, x, y, u, nk, su, al, be, hb, st);
+}
+
+template <int SD, typename C, bool PEEL>
+static void launch_rows_auto(const void* A, const void* x, void* y, int64_t u, int64_t nk,
+                             int64_t su, C al, C be, int hb, cudaStream_t st) {
+  constexpr int VEC = VecN<SD>::N;
+  const int64_t nunits = std::max<int64_t>(1, nk / VEC);
+  int G = pick_row_group(nunits, 16);
+  int RS = pick_row_steps(nunits, G, kRowBatch);
+  if ((size_t)nk * sizeof(C) > 96 * 1024) G = 32, RS = 1;  // x stays in L1, not smem
+  switch (G) {
+    case 32: rows_by_steps<SD, C, 32, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 16: rows_by_steps<SD, C, 16, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 8: rows_by_steps<SD, C, 8, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 4: rows_by_steps<SD, C, 4, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 2: rows_by_steps<SD, C, 2, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
+    default: rows_by_steps<SD, C, 1, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
+  }
+}
+
+template <int SD, typename C>
+static void launch_staged(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t v,
+                          C al, C be, int hb, cudaStream_t st) {
+  using T = typename St<SD>::T;
+  constexpr int VEC = VecN<SD>::N;
+  const int64_t slab_bytes = nk * v * (int64_t)sizeof(T);
+  const int spt = (int)std::max<int64_t>(1, std::min<int64_t>(kStageBytes / slab_bytes, u));
+  const int64_t ntiles = cdiv(u, spt);
+  const bool vrow = v == 1 && (slab_bytes % 16) == 0;
+  const int64_t units = vrow ? nk / VEC : nk;
+  const int64_t outs = (int64_t)spt * v;
+  int G = 1;  // idle threads split each output's j range
+  while (G < 8 && outs * G * 2 <= kThreads && G * 2 <= units) G <<= 1;
+  const size_t smem = (size_t)cdiv(nk * (int64_t)sizeof(C), 16) * 16 + 2 * (kStageBytes + 16) +
+                      kThreads * sizeof(C);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, 6LL * sm_count());
+  if (vrow) {
+    auto kern = k_staged<SD, C, true>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, spt,
+                                       ntiles, G, al, be, hb);
+  } else {
+    auto kern = k_staged<SD, C, false>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, spt,
+                                       ntiles, G, al, be, hb);
+  }
+}
+
+template <int SD, typename C, bool AL>
+static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t v,
+                       int64_t su, int64_t sk, C al, C be, int hb, cudaStream_t st) {
+  using T = typename St<SD>::T;
+  constexpr int VEC = VecN<SD>::N;
+  constexpr int UA_UNR = VEC >= 8 ? 2 : 4;  // scalar loads in flight: UNR * VEC
+  const int64_t stripes = cdiv(v, 32 * VEC);
+  const int JR = pick_col_phases(nk, stripes, u);
+  const int64_t ntile = cdiv(stripes, kWarps / JR);
+  const int64_t blocks = u * ntile;
+  if (blocks > 0x7fffffffLL) return set_error(TV_EKERNEL, "tv_tvc: view too large for COLS grid");
+  const T* At = (const T*)A;
+  const T* xt = (const T*)x;
+  T* yt = (T*)y;
+  const unsigned b = (unsigned)blocks;
+  switch (JR) {
+    case 1: k_cols<SD, C, 1, AL ? 8 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
+    case 2: k_cols<SD, C, 2, AL ? 8 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
+    case 4: k_cols<SD, C, 4, AL ? 4 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
+    default: k_cols<SD, C, 8, AL ? 4 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
+  }
+  return TV_OK;
 }
 
 template <int SD, typename C>
 static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su, int64_t sk,
                      const void* x, double alpha, double beta, void* y, cudaStream_t st,
-                     int force_generic) {
+                     int naive) {
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
   const C al = (C)alpha, be = (C)beta;
   const int hb = beta != 0.0;
   if (u == 0 || v == 0) return TV_OK;
-  const int reg = force_generic ? REG_GENERIC : regime_of(A, SD, u, nk, v);
+  const int reg = naive ? REG_GENERIC : regime_strided(A, (int)sizeof(T), u, nk, v, su, sk);
+  int rc = TV_OK;
   switch (reg) {
-    case REG_ROWS: {
-      const int G = pick_row_group(nk / VEC);
-      if (G == 32) launch_rows<SD, C, 32>(A, x, y, u, nk, al, be, hb, st);
-      else if (G == 16) launch_rows<SD, C, 16>(A, x, y, u, nk, al, be, hb, st);
-      else if (G == 8) launch_rows<SD, C, 8>(A, x, y, u, nk, al, be, hb, st);
-      else launch_rows<SD, C, 4>(A, x, y, u, nk, al, be, hb, st);
+    case REG_ROWS:
+      launch_rows_auto<SD, C, false>(A, x, y, u, nk, su, al, be, hb, st);
       break;
-    }
+    case REG_ROWS_U:
+      launch_rows_auto<SD, C, true>(A, x, y, u, nk, su, al, be, hb, st);
+      break;
+    case REG_STAGED:
+      launch_staged<SD, C>(A, x, y, u, nk, v, al, be, hb, st);
+      break;
     case REG_ROWS_SHORT: {
       constexpr int UNR = 4;
       const int nkv = (int)(nk / VEC);
-      const int64_t rows_per_block = (kThreads / 32) * (32 / nkv) * UNR;
+      const int64_t rows_per_block = kWarps * (32 / nkv) * UNR;
       const unsigned grid = grid_for(u, rows_per_block, 32);
       k_rows_short<SD, C, UNR>
-          <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, al, be, hb);
+          <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, su, al, be, hb);
       break;
     }
-    case REG_COLS: {
-      constexpr int UNR = 4;
-      const int64_t ntile = cdiv(v / VEC, 32);
-      const int64_t blocks = u * ntile;
-      if (blocks > 0x7fffffffLL) return set_error(TV_EKERNEL, "tv_tvc: view too large for COLS grid");
-      k_cols<SD, C, UNR><<<(unsigned)blocks, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u,
-                                                                nk, v, ntile, al, be, hb);
+    case REG_COLS:
+      rc = launch_cols<SD, C, true>(A, x, y, u, nk, v, su, sk, al, be, hb, st);
       break;
-    }
+    case REG_COLS_U:
+      rc = launch_cols<SD, C, false>(A, x, y, u, nk, v, su, sk, al, be, hb, st);
+      break;
     case REG_SLABS: {
-      constexpr int UNR = 4;
-      const unsigned grid = grid_for(u, kThreads / 32, 32);
-      k_slabs<SD, C, UNR>
-          <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, (int)v, al, be, hb);
+      const unsigned grid = grid_for(u, kWarps, 32);
+      k_slabs<SD, C, 4, true><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk,
+                                                         (int)v, su, sk, al, be, hb);
+      break;
+    }
+    case REG_SLABS_U: {
+      const unsigned grid = grid_for(u, kWarps, 32);
+      k_slabs<SD, C, 8, false><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk,
+                                                          (int)v, su, sk, al, be, hb);
       break;
     }
     default: {
       if (v == 1) {
-        const unsigned grid = grid_for(u, kThreads / 32, 32);
-        k_generic_rows<SD, C>
+        const unsigned grid = grid_for(u, kWarps, 32);
+        k_naive_rows<SD, C>
             <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, sk, al, be, hb);
       } else {
         const unsigned grid = grid_for(u * v, kThreads, 32);
-        k_generic_cols<SD, C><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, v,
-                                                         su, sk, al, be, hb);
+        k_naive_cols<SD, C><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, v,
+                                                       su, sk, al, be, hb);
       }
     }
   }
+  if (rc != TV_OK) return rc;
   return check_launch("tv_tvc");
 }
 
 int tvc_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                  int64_t su, int64_t sk, const void* x, double alpha, double beta, void* y,
-                 void* stream, int force_generic) {
+                 void* stream, int naive) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (mode_id(storage, compute)) {
     case MODE_F64:
-      return tvc_typed<TV_F64, double>(A, u, nk, v, su, sk, x, alpha, beta, y, st, force_generic);
+      return tvc_typed<TV_F64, double>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
     case MODE_F32:
-      return tvc_typed<TV_F32, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, force_generic);
+      return tvc_typed<TV_F32, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
     case MODE_F32F64:
-      return tvc_typed<TV_F32, double>(A, u, nk, v, su, sk, x, alpha, beta, y, st, force_generic);
+      return tvc_typed<TV_F32, double>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
     case MODE_F16F32:
-      return tvc_typed<TV_F16, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, force_generic);
+      return tvc_typed<TV_F16, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
     case MODE_BF16F32:
-      return tvc_typed<TV_BF16, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, force_generic);
+      return tvc_typed<TV_BF16, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
     default:
       return set_error(TV_EMODE, "invalid (storage, compute) pair");
   }
@@ -485,14 +900,12 @@ extern "C" int tv_getvc(int trans, const void* A, int storage, int compute, int6
   if (trans == 0) {  // matvec: y[i] = sum_j A[i*lda + j] x[j]
     if (m == 0) return TV_OK;
     if (n == 0) return tv::set_error(TV_EKERNEL, "tv_getvc: empty contraction");
-    return tv::tvc_dispatch(A, storage, compute, m, n, 1, lda, 1, x, alpha, beta, y, stream,
-                            lda != n);
+    return tv::tvc_dispatch(A, storage, compute, m, n, 1, lda, 1, x, alpha, beta, y, stream, 0);
   }
   if (trans == 1) {  // vecmat: y[c] = sum_i x[i] A[i*lda + c]
     if (n == 0) return TV_OK;
     if (m == 0) return tv::set_error(TV_EKERNEL, "tv_getvc: empty contraction");
-    return tv::tvc_dispatch(A, storage, compute, 1, m, n, 0, lda, x, alpha, beta, y, stream,
-                            lda != n);
+    return tv::tvc_dispatch(A, storage, compute, 1, m, n, 0, lda, x, alpha, beta, y, stream, 0);
   }
   return tv::set_error(TV_EKERNEL, "tv_getvc: trans must be 0 (matvec) or 1 (vecmat)");
 }

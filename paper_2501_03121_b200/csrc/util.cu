@@ -239,18 +239,21 @@ __global__ void k_fill(typename St<SD>::T* __restrict__ A, int64_t total, int ki
 // whole buffer hits a magic value, which keeps the loads alive)
 __global__ void __launch_bounds__(256) k_read_stream(const uint4* __restrict__ p, int64_t n16,
                                                      uint32_t* __restrict__ sink) {
+  // each CTA streams one contiguous chunk, 8 x 4 KB in flight per pass
   constexpr int UNR = 8;
   uint32_t acc = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + (UNR - 1) * stride < n16; i += UNR * stride) {
+  const int64_t chunk = ((n16 + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n16 ? lo + chunk : n16;
+  int64_t i = lo + threadIdx.x;
+  for (; i + (UNR - 1) * 256 < hi; i += UNR * 256) {
     uint4 v[UNR];
 #pragma unroll
-    for (int t = 0; t < UNR; ++t) v[t] = ld_stream16(p + i + t * stride);
+    for (int t = 0; t < UNR; ++t) v[t] = ld_stream16(p + i + t * 256);
 #pragma unroll
     for (int t = 0; t < UNR; ++t) acc ^= v[t].x ^ v[t].y ^ v[t].z ^ v[t].w;
   }
-  for (; i < n16; i += stride) {
+  for (; i < hi; i += 256) {
     const uint4 v = ld_stream16(p + i);
     acc ^= v.x ^ v.y ^ v.z ^ v.w;
   }

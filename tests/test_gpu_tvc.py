@@ -98,16 +98,29 @@ REGIME_CASES = [
     # so regimes are asserted for f32 storage only
     ((64, 256), 1, "rows"),
     ((300, 96), 1, "rows"),
-    ((96, 96, 12), 2, "rows_short"),
-    ((5000, 8), 1, "rows_short"),
+    ((300, 160), 1, "rows"),
+    ((96, 96, 12), 2, "rows"),
+    ((5000, 8), 1, "rows"),
+    ((1, 8), 1, "rows"),
     ((256, 256), 0, "cols"),
     ((7, 40, 256), 1, "cols"),
     ((96, 96, 12), 1, "slabs"),
     ((33, 17, 48), 1, "slabs"),
-    ((5, 7, 3), 1, "generic"),
-    ((9, 13), 1, "generic"),
+    ((33, 17, 9), 1, "staged"),
+    ((3, 200, 48), 1, "slabs"),
+    ((4, 300, 21), 1, "slabs_u"),
+    ((5, 7, 3), 1, "staged"),
+    ((9, 13), 1, "staged"),
     ((1, 1024, 1), 1, "rows"),
-    ((2, 3), 0, "generic"),
+    ((2, 3), 0, "slabs_u"),
+    ((13, 13, 13, 13), 3, "staged"),
+    ((13, 13, 13, 13), 2, "staged"),
+    ((999, 7, 5), 2, "staged"),
+    ((61, 130, 1), 1, "rows_u"),
+    ((77, 330), 1, "rows_u"),
+    ((7, 19, 979), 1, "cols_u"),
+    ((3, 979, 41), 1, "cols_u"),
+    ((30, 1001), 1, "rows_u"),
 ]
 
 
@@ -144,11 +157,11 @@ def test_regimes_float_data(tv, mode_name):
                                y.buf.view(torch.uint8) if y.buf.dtype != torch.uint16 else y.buf.view(torch.int16))
 
 
-def test_misaligned_view_uses_generic(tv):
+def test_misaligned_view_uses_unaligned_rows(tv):
     base = torch.arange(1.0, 1.0 + 4 * 64 + 1, dtype=torch.float32, device="cuda")
     buf = base[1:]  # 4-byte offset: not 16-byte aligned
     t = tv.Tensor(tv.Shape((4, 64)), buf, tv.F32)
-    assert tv.tvc_regime(t, 1) == "generic"
+    assert tv.tvc_regime(t, 1) == "rows_u"
     x = np.arange(64, dtype=np.float32) % 5
     y = tv.tvc_native(t, x, 1)
     want = O.tvc(buf.cpu().numpy(), (4, 64), x, 1, "f32")

@@ -172,11 +172,18 @@ def test_library_argument_validation_without_gpu():
     assert lib.tv_fill(None, 0, 0, 1, ext, 3, 1, 2, 1, None) == 1
     # regime choice is host logic: aligned fake pointers, no dereference
     p = 1 << 20
-    assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 1       # rows
-    assert lib.tv_tvc_regime(p, 1, 1000, 12, 1) == 2       # short rows
+    assert lib.tv_tvc_regime(p, 1, 1000, 256, 1) == 1      # rows
+    assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 1       # aligned short rows stay rows
+    assert lib.tv_tvc_regime(p, 1, 1000, 12, 1) == 1
     assert lib.tv_tvc_regime(p, 1, 1, 2048, 4096) == 3     # columns
-    assert lib.tv_tvc_regime(p, 1, 1000, 96, 12) == 4      # narrow slabs
-    assert lib.tv_tvc_regime(p + 4, 1, 1000, 96, 12) == 0  # misaligned -> generic
+    assert lib.tv_tvc_regime(p, 1, 1000, 96, 12) == 4      # small aligned slabs
+    assert lib.tv_tvc_regime(p, 1, 1000, 13, 1) == 8       # unaligned short rows -> staged
+    assert lib.tv_tvc_regime(p, 0, 1000, 13, 13) == 8      # unaligned small slabs -> staged
+    assert lib.tv_tvc_regime(p, 1, 1000, 200, 48) == 4     # narrow slabs
+    assert lib.tv_tvc_regime(p + 4, 1, 1000, 96, 12) == 7  # misaligned -> scalar slabs
+    assert lib.tv_tvc_regime(p, 0, 1000, 13, 1) == 8       # odd fp64 rows -> staged
+    assert lib.tv_tvc_regime(p, 0, 1000, 131, 1) == 5      # odd fp64 long rows -> scalar rows
+    assert lib.tv_tvc_regime(p, 0, 9, 979, 979) == 6       # odd fp64 columns -> scalar columns
 
 
 def test_no_oracle_import_in_product():
