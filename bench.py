@@ -170,6 +170,11 @@ def cpu_reference(workload: str, budget_s: float = 12.0) -> dict:
         def once():
             for k in range(d):
                 O.tvc(vals, shape, xs[k], k, mode)
+    try:  # torchrun sets OMP_NUM_THREADS=1; the reference arm uses every host core
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        pass
     once()  # warm-up
     times = []
     t_end = time.perf_counter() + budget_s
@@ -256,26 +261,13 @@ def run_ours(args) -> dict | None:
     if wl.get("flush"):
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * d + 2)] for _ in range(args.steps)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
 
-    def step(evs=None):
-        if evs is not None:
-            evs[0].record()
-        outs = []
-        for k in range(d):
-            if evs is not None:
-                evs[1 + 2 * k].record()
-            res = tv.dtvc(dt, xs[k], k, defer=(k == s and world > 1))
-            if evs is not None:
-                evs[2 + 2 * k].record()
-            if k == s and world > 1:
-                local_out = res.parts[me]
-                group.all_reduce_sum(rank, local_out.buf)
-                res = tv.DistributedTensor(res.plan, [local_out])
-            outs.append(res)
-        if evs is not None:
-            evs[2 * d + 1].record()
-        return outs
+    def step():
+        # one mode sweep through the public API; at N > 1 the split-mode
+        # reduction runs on a side stream under the other modes' streaming
+        return tv.dtvc_sweep(dt, xs)
 
     for _ in range(args.warmup):
         step()
@@ -289,13 +281,14 @@ def run_ours(args) -> dict | None:
     for i in range(args.steps):
         if flush is not None:
             flush.zero_()
-        step(ev[i])
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
-    step_ms = [ev[i][0].elapsed_time(ev[i][2 * d + 1]) for i in range(args.steps)]
-    kern_ms = [[ev[i][1 + 2 * k].elapsed_time(ev[i][2 + 2 * k]) for i in range(args.steps)] for k in range(d)]
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -304,6 +297,21 @@ def run_ours(args) -> dict | None:
     job_bytes_step = sum(mode_bytes) * world  # slabs are even for the configured shapes
     ms_per_step = total_ms / args.steps
     value = job_bytes_step / (ms_per_step / 1e3) / 1e9
+
+    # per-kernel durations (the roofline): each mode's tv_tvc launch alone,
+    # event-timed on its stream, same inputs, after the timed region
+    kern_ms = [[] for _ in range(d)]
+    for _ in range(max(3, min(args.steps, 10))):
+        for k in range(d):
+            if flush is not None:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            tv.dtvc(dt, xs[k], k, defer=(k == s and world > 1))
+            e1.record()
+            kern_ms[k].append((e0, e1))
+    torch.cuda.synchronize()
+    kern_ms = [[a.elapsed_time(b) for a, b in v] for v in kern_ms]
 
     # dominant kernel: the mode with the largest time share
     avg_k = [statistics.fmean(v) for v in kern_ms]
@@ -354,6 +362,7 @@ def run_ours(args) -> dict | None:
         "comm_bytes_per_step_per_gpu": comm_bytes,
         "e2e": e2e,
         "gpu_launches": args.steps * (d + (1 if world > 1 else 0)),
+        "step_overlap": "split-mode reduction on a side stream under the other modes" if world > 1 else None,
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -412,12 +421,11 @@ def run_e2e_sweep(args, tv, dt, part, xs, s, world, rank, group, job_bytes_step)
         nonlocal d2h
         part.buf.copy_(host, non_blocking=True)
         xd = [x.cuda(non_blocking=True) for x in xh]
+        res = tv.dtvc_sweep(dt, xd)
         outs = []
         for k in range(d):
-            res = tv.dtvc(dt, xd[k], k, defer=(k == s and world > 1))
-            if k == s and world > 1:
-                group.all_reduce_sum(rank, res.parts[me].buf)
-            outs.append(res.parts[me].buf.cpu())
+            local = next(p for p in res[k].parts if p is not None)
+            outs.append(local.buf.cpu())
         d2h = sum(o.numel() * o.element_size() for o in outs)
         return outs
 
