@@ -70,10 +70,13 @@ struct Unit {
 // (odd extents such as 979 or 175 in fp64): the elements before its first
 // 16-byte boundary (head) and after its last full vector (tail) are folded by
 // scalar loads, so the body still streams as full vectors.
-// Every lane issues QB loads per batch (one memory round trip): a batch walks
-// QB vectors of one row (RS = 1, long rows) or QB / RS vectors of each of RS
-// row steps (short rows).
-template <int SD, typename C, int G, int RS, int QB, bool XS, bool PEEL>
+// Every lane issues QB loads per batch (one memory round trip): LONG rows
+// loop over batches of QB vectors of one row; short rows (at most QB / RS
+// vectors per lane) take ONE batch covering RS row steps, idle slots loading
+// a clamped in-range vector so the batch issues without predicates.
+// G (chosen on the host) trades the 128-byte-line count of a warp load
+// (G >= 8) against the log2(G) shuffle levels each row's sum costs.
+template <int SD, typename C, int G, int RS, int QB, bool XS, bool PEEL, bool LONG>
 __global__ void __launch_bounds__(kThreads)
     k_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
            typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t su, C alpha, C beta,
@@ -121,21 +124,36 @@ __global__ void __launch_bounds__(kThreads)
     for (int r2 = 0; r2 < RS; ++r2)
 #pragma unroll
       for (int e = 0; e < VEC; ++e) acc[r2][e] = C(0);
-    if constexpr (RS == 1) {
+    if constexpr (LONG) {  // rows of more than QB vectors per lane: batched loop
       const int64_t row = row0 + rs;
       if (row < u) {
         const T* rp = A + row * su;
         const int64_t h = head_of(rp);
         const int64_t nb = (nk - h) / VEC;
         const uint4* body = reinterpret_cast<const uint4*>(rp + h);
-        // full batches without predicates, so all QPL loads issue back to back
+        // full batches without predicates, register double-buffered: batch
+        // b + 1 is in flight while batch b folds
         int64_t q0 = g;
-        for (; q0 + (int64_t)(QPL - 1) * G < nb; q0 += (int64_t)G * QPL) {
-          uint4 buf[QPL];
+        const int64_t step = (int64_t)G * QPL;
+        if (q0 + (int64_t)(QPL - 1) * G < nb) {
+          uint4 cur[QPL];
 #pragma unroll
-          for (int t = 0; t < QPL; ++t) buf[t] = ld_stream16(body + q0 + (int64_t)t * G);
+          for (int t = 0; t < QPL; ++t) cur[t] = ld_stream16(body + q0 + (int64_t)t * G);
+          for (;;) {
+            const int64_t qn = q0 + step;
+            const bool more = qn + (int64_t)(QPL - 1) * G < nb;
+            uint4 nxt[QPL];
+            if (more) {
 #pragma unroll
-          for (int t = 0; t < QPL; ++t) fold_vec(buf[t], h + (q0 + (int64_t)t * G) * VEC, acc[0]);
+              for (int t = 0; t < QPL; ++t) nxt[t] = ld_stream16(body + qn + (int64_t)t * G);
+            }
+#pragma unroll
+            for (int t = 0; t < QPL; ++t) fold_vec(cur[t], h + (q0 + (int64_t)t * G) * VEC, acc[0]);
+            q0 = qn;
+            if (!more) break;
+#pragma unroll
+            for (int t = 0; t < QPL; ++t) cur[t] = nxt[t];
+          }
         }
         for (; q0 < nb; q0 += G) fold_vec(ld_stream16(body + q0), h + q0 * VEC, acc[0]);
         if constexpr (PEEL) acc[0][0] += fold_edges(rp, h, nb);
@@ -277,12 +295,37 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int e = 0; e < VEC; ++e) acc[e] = fma(a[e], xj, acc[e]);
       };
-      for (; j0 + (int64_t)(UNR - 1) * JR < nk; j0 += (int64_t)JR * UNR) {
-        uint4 buf[UNR];
+      // long columns (JR > 1): register double buffer, batch b + 1 in flight
+      // while batch b folds; short ones keep the lighter single-buffer loop
+      // (occupancy matters more there)
+      const int64_t step = (int64_t)JR * UNR;
+      if constexpr (JR == 1) {
+        for (; j0 + (int64_t)(UNR - 1) * JR < nk; j0 += step) {
+          uint4 buf[UNR];
 #pragma unroll
-        for (int t = 0; t < UNR; ++t) buf[t] = ld_stream16(cb + (j0 + (int64_t)t * JR) * sk);
+          for (int t = 0; t < UNR; ++t) buf[t] = ld_stream16(cb + (j0 + (int64_t)t * JR) * sk);
 #pragma unroll
-        for (int t = 0; t < UNR; ++t) fold(buf[t], j0 + (int64_t)t * JR);
+          for (int t = 0; t < UNR; ++t) fold(buf[t], j0 + (int64_t)t * JR);
+        }
+      } else if (j0 + (int64_t)(UNR - 1) * JR < nk) {
+        uint4 cur[UNR];
+#pragma unroll
+        for (int t = 0; t < UNR; ++t) cur[t] = ld_stream16(cb + (j0 + (int64_t)t * JR) * sk);
+        for (;;) {
+          const int64_t jn = j0 + step;
+          const bool more = jn + (int64_t)(UNR - 1) * JR < nk;
+          uint4 nxt[UNR];
+          if (more) {
+#pragma unroll
+            for (int t = 0; t < UNR; ++t) nxt[t] = ld_stream16(cb + (jn + (int64_t)t * JR) * sk);
+          }
+#pragma unroll
+          for (int t = 0; t < UNR; ++t) fold(cur[t], j0 + (int64_t)t * JR);
+          j0 = jn;
+          if (!more) break;
+#pragma unroll
+          for (int t = 0; t < UNR; ++t) cur[t] = nxt[t];
+        }
       }
       for (; j0 < nk; j0 += JR) fold(ld_stream16(cb + j0 * sk), j0);
     } else {
@@ -595,33 +638,21 @@ static unsigned grid_for(int64_t work_items, int64_t per_block, int waves_cap) {
 
 static int64_t waste_of(int64_t n, int G) { return cdiv(n, G) * G - n; }
 
-// Lanes per row.  A warp load instruction costs one L1 wavefront per 128-byte
-// line it touches, so a row's lanes must cover >= 128 contiguous bytes per
-// instruction (G * unit_bytes >= 128): short rows take G = pow2ceil(units)
-// (idle lanes, but adjacent rows stay contiguous); long rows the widest
-// G >= gmin idling at most 1/8 of the unit slots, else the fewest.
-static int pick_row_group(int64_t nunits, int unit_bytes) {
-  if (nunits <= 32) {
+// Lanes per row (units = 16-byte vectors).  A warp load costs one L1
+// wavefront per 128-byte line it touches, so each row segment should be
+// >= 128 bytes (G >= 8); every extra lane costs a shuffle level per row.
+// Measured on B200 (C3/C4 short rows, C2 long rows): rows of <= 8 vectors
+// take pow2ceil(units) lanes (adjacent rows stay contiguous), up to 32
+// vectors 8 lanes, up to 64 vectors 16, longer rows the full warp.
+static int pick_row_group(int64_t nunits) {
+  if (nunits <= 8) {
     int G = 1;
     while (G < nunits) G <<= 1;
     return G;
   }
-  const int gmin = std::max(1, std::min(32, 128 / unit_bytes));
-  int best = 32;
-  for (int G : {32, 16, 8, 4, 2, 1}) {
-    if (G < gmin) break;
-    if (waste_of(nunits, G) * 8 <= nunits) return G;
-    if (waste_of(nunits, G) < waste_of(nunits, best)) best = G;
-  }
-  return best;
-}
-
-// row steps per batch so a lane keeps QB loads in flight on short rows
-static int pick_row_steps(int64_t nunits, int G, int qb) {
-  const int64_t qpl = cdiv(nunits, G);
-  if (qpl * 4 <= qb) return 4;
-  if (qpl * 2 <= qb) return 2;
-  return 1;
+  if (nunits <= 32) return 8;
+  if (nunits <= 64) return 16;
+  return 32;
 }
 
 // row phases of the COLS kernel: enough rows per warp for deep load
@@ -672,6 +703,9 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
     if (stageable && nk * sb <= kStagedRowBytes) return REG_STAGED;
     return REG_ROWS_U;
   }
+  // small aligned slabs with short columns (n_k <= 32) leave COLS/SLABS warps
+  // too little work per slab: staged tiles win there (paper d = 9, 10 tensors)
+  if (al_cols && stageable && nk <= 32 && nk * v * sb <= kStageBytes / 2) return REG_STAGED;
   if (al_cols) return (v / VEC >= 32) ? REG_COLS : REG_SLABS;
   if (stageable && nk * v * sb <= kStageBytes / 2) return REG_STAGED;
   return v >= 32 ? REG_COLS_U : REG_SLABS_U;
@@ -686,7 +720,7 @@ int regime_of(const void* A, int storage, int64_t u, int64_t nk, int64_t v) {
 
 constexpr int kRowBatch = 4;  // 16-byte loads per lane per batch
 
-template <int SD, typename C, int G, int RS, bool PEEL>
+template <int SD, typename C, int G, int RS, bool PEEL, bool LONG>
 static void launch_rows(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t su,
                         C al, C be, int hb, cudaStream_t st) {
   using T = typename St<SD>::T;
@@ -694,23 +728,24 @@ static void launch_rows(const void* A, const void* x, void* y, int64_t u, int64_
   const int64_t rows_per_block = (int64_t)kWarps * (32 / G) * RS;
   const unsigned grid = grid_for(u, rows_per_block, 32);
   if (xs_bytes <= 96 * 1024) {
-    auto kern = k_rows<SD, C, G, RS, kRowBatch, true, PEEL>;
+    auto kern = k_rows<SD, C, G, RS, kRowBatch, true, PEEL, LONG>;
     if (xs_bytes > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs_bytes);
     kern<<<grid, kThreads, xs_bytes, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
-  } else if constexpr (G == 32 && RS == 1) {
+  } else if constexpr (G == 32 && RS == 1 && LONG) {
     // rows longer than the shared-memory copy of x: x through L1
-    k_rows<SD, C, 32, 1, kRowBatch, false, PEEL>
+    k_rows<SD, C, 32, 1, kRowBatch, false, PEEL, true>
         <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
   }
 }
 
 template <int SD, typename C, int G, bool PEEL>
-static void rows_by_steps(int RS, const void* A, const void* x, void* y, int64_t u, int64_t nk,
-                          int64_t su, C al, C be, int hb, cudaStream_t st) {
-  if (RS == 4) launch_rows<SD, C, G, 4, PEEL>(A, x, y, u, nk, su, al, be, hb, st);
-  else if (RS == 2) launch_rows<SD, C, G, 2, PEEL>(A, x, y, u, nk, su, al, be, hb, st);
-  else launch_rows<SD, C, G, 1, PEEL>(A, x, y, u, nk, su, al, be, hb, st);
+static void rows_by_steps(int RS, bool lng, const void* A, const void* x, void* y, int64_t u,
+                          int64_t nk, int64_t su, C al, C be, int hb, cudaStream_t st) {
+  if (lng) launch_rows<SD, C, G, 1, PEEL, true>(A, x, y, u, nk, su, al, be, hb, st);
+  else if (RS == 4) launch_rows<SD, C, G, 4, PEEL, false>(A, x, y, u, nk, su, al, be, hb, st);
+  else if (RS == 2) launch_rows<SD, C, G, 2, PEEL, false>(A, x, y, u, nk, su, al, be, hb, st);
+  else launch_rows<SD, C, G, 1, PEEL, false>(A, x, y, u, nk, su, al, be, hb, st);
 }
 
 template <int SD, typename C, bool PEEL>
@@ -718,16 +753,18 @@ static void launch_rows_auto(const void* A, const void* x, void* y, int64_t u, i
                              int64_t su, C al, C be, int hb, cudaStream_t st) {
   constexpr int VEC = VecN<SD>::N;
   const int64_t nunits = std::max<int64_t>(1, nk / VEC);
-  int G = pick_row_group(nunits, 16);
-  int RS = pick_row_steps(nunits, G, kRowBatch);
-  if ((size_t)nk * sizeof(C) > 96 * 1024) G = 32, RS = 1;  // x stays in L1, not smem
+  int G = pick_row_group(nunits);
+  const int64_t qpl = cdiv(nunits, G);
+  bool lng = qpl > kRowBatch;
+  int RS = lng ? 1 : (qpl * 4 <= kRowBatch ? 4 : qpl * 2 <= kRowBatch ? 2 : 1);
+  if ((size_t)nk * sizeof(C) > 96 * 1024) G = 32, RS = 1, lng = true;  // x stays in L1, not smem
   switch (G) {
-    case 32: rows_by_steps<SD, C, 32, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
-    case 16: rows_by_steps<SD, C, 16, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
-    case 8: rows_by_steps<SD, C, 8, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
-    case 4: rows_by_steps<SD, C, 4, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
-    case 2: rows_by_steps<SD, C, 2, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
-    default: rows_by_steps<SD, C, 1, PEEL>(RS, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 32: rows_by_steps<SD, C, 32, PEEL>(RS, lng, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 16: rows_by_steps<SD, C, 16, PEEL>(RS, lng, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 8: rows_by_steps<SD, C, 8, PEEL>(RS, lng, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 4: rows_by_steps<SD, C, 4, PEEL>(RS, lng, A, x, y, u, nk, su, al, be, hb, st); break;
+    case 2: rows_by_steps<SD, C, 2, PEEL>(RS, lng, A, x, y, u, nk, su, al, be, hb, st); break;
+    default: rows_by_steps<SD, C, 1, PEEL>(RS, lng, A, x, y, u, nk, su, al, be, hb, st); break;
   }
 }
 

@@ -105,7 +105,8 @@ REGIME_CASES = [
     ((256, 256), 0, "cols"),
     ((7, 40, 256), 1, "cols"),
     ((96, 96, 12), 1, "slabs"),
-    ((33, 17, 48), 1, "slabs"),
+    ((33, 17, 48), 1, "staged"),
+    ((33, 40, 48), 1, "slabs"),
     ((33, 17, 9), 1, "staged"),
     ((3, 200, 48), 1, "slabs"),
     ((4, 300, 21), 1, "slabs_u"),
