@@ -110,15 +110,20 @@ def device_fold(srcs: list[torch.Tensor], dst: torch.Tensor, *, mixed: bool,
 
 
 def device_fold_strided(recv: torch.Tensor, stride: int, p: int, n: int, dst: torch.Tensor, *,
-                        mixed: bool, mode: PrecisionMode | None, start: int) -> None:
-    """Fold p contributions laid out back to back in one receive buffer."""
+                        mixed: bool, mode: PrecisionMode | None, start: int, chunk: int = 0) -> None:
+    """Fold p contributions laid out back to back in one receive buffer: one
+    ring chunk starting at rank `start` (chunk = 0), or whole buffers whose
+    chunk c (of `chunk` elements) starts at rank c."""
     if n == 0:
         return
     st, ct = _pair_for(dst, mode)
     lib = _lib.load()
-    _lib.check(lib.tv_rank_fold_strided(recv.data_ptr(), stride, p, n, 0, start, st, ct,
+    _lib.check(lib.tv_rank_fold_strided(recv.data_ptr(), stride, p, n, chunk, start, st, ct,
                                         int(mixed), dst.data_ptr(), _lib.stream_ptr()),
                "rank fold")
+
+
+SMALL_GATHER_BYTES = 1 << 20
 
 
 def _check_lengths(bufs) -> int:
@@ -359,6 +364,14 @@ class RankGroup:
             return
         if self.algo == "nccl" and not mixed:
             dist.all_reduce(buf, group=self.group)
+            return
+        if n * buf.element_size() * p <= SMALL_GATHER_BYTES:
+            # latency-bound sizes (dHOPM3 vectors): one all-gather of every
+            # rank's buffer, then each rank folds all ring chunks itself --
+            # the same values in the same order, one NCCL call instead of two
+            everyone = torch.empty(p * n, dtype=buf.dtype, device=buf.device)
+            dist.all_gather_into_tensor(_wire(everyone), _wire(buf.contiguous()), group=self.group)
+            self.fold(everyone, n, p, n, buf, mixed=mixed, mode=mode, start=0, chunk=sizes[0])
             return
         mine = sizes[rank]
         recv = torch.empty(p * mine, dtype=buf.dtype, device=buf.device)

@@ -140,6 +140,22 @@ def test_dtvc_examples_and_errors(tv):
         tv.dtvc(tv.distribute(t, 0, 2), np.ones(5), 0)
 
 
+@pytest.mark.parametrize("name", ["f64", "bf16f32"])
+def test_dtvc_sweep_equals_individual_contractions(tv, name):
+    mode = tv.MODES[name]
+    shape = tv.Shape((9, 8, 10, 6))
+    for s in (0, 2):
+        for p in (1, 3):
+            dt = tv.distribute_generated(shape, s, p, mode, fill="hash", seed=11)
+            xs = [O.demote((np.arange(n) % 5) + 1.0, name).copy() for n in shape.extents]
+            res = tv.dtvc_sweep(dt, xs)
+            assert sorted(res) == [0, 1, 2, 3]
+            for k in range(4):
+                want = tv.undistribute(tv.dtvc(dt, xs[k], k)).to_numpy()
+                got = tv.undistribute(res[k]).to_numpy()
+                assert np.array_equal(_bits(got), _bits(want)), (s, p, k)
+
+
 @pytest.mark.parametrize("name", ["f16f32", "bf16f32", "f32f64"])
 def test_dtvc_mixed_reduction_bitwise(tv, name):
     mode = tv.MODES[name]

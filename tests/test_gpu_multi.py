@@ -49,16 +49,28 @@ def _worker(rank, world, port, q):
             for s in sorted({2} | ({4} if tv.make_split_plan(4, 4, world).p_eff == world else set())):
                 dt = tv.distribute_generated(tv.Shape(shape), s, world, mode, fill="hash", seed=4, group=group)
                 parts, ranges = O.split(host, s, world)
+                xs = [O.demote((np.arange(shape[k]) % 5) + 1.0, name).copy() for k in range(5)]
+                sweep = tv.dtvc_sweep(dt, xs)
                 for k in range(5):
-                    x = O.demote((np.arange(shape[k]) % 5) + 1.0, name).copy()
+                    x = xs[k]
                     res = tv.dtvc(dt, x, k)
                     kind, outs, s2 = O.dtvc(parts, ranges, s, x, k, name)
-                    if k == s:
-                        got = res.parts[0].to_numpy()
-                        ok.append((name, s, k, bool(np.array_equal(_bits(got), _bits(outs[0].reshape(-1))))))
-                    else:
-                        got = res.parts[rank].to_numpy()
-                        ok.append((name, s, k, bool(np.array_equal(_bits(got), _bits(outs[rank].reshape(-1))))))
+                    want = outs[0] if k == s else outs[rank]
+                    for tag, r in (("dtvc", res), ("sweep", sweep[k])):
+                        got = (r.parts[0] if k == s else r.parts[rank]).to_numpy()
+                        ok.append((name, s, k, tag, bool(np.array_equal(_bits(got), _bits(want.reshape(-1))))))
+        # a reduction above the small-gather threshold: all-to-all + fold + all-gather
+        big = (64, 64, 2 * world, 64)
+        fullb = O.fill_values(big, "hash", seed=6).reshape(big)
+        for name in ("f32", "bf16f32"):
+            mode = tv.MODES[name]
+            hostb = O.demote(fullb.reshape(-1), name).reshape(big)
+            dt = tv.distribute_generated(tv.Shape(big), 2, world, mode, fill="hash", seed=6, group=group)
+            x = O.demote((np.arange(big[2]) % 3) + 1.0, name).copy()
+            parts, ranges = O.split(hostb, 2, world)
+            _, outs, _ = O.dtvc(parts, ranges, 2, x, 2, name)
+            got = tv.dtvc(dt, x, 2).parts[0].to_numpy()
+            ok.append((name, "big-reduce", 2, bool(np.array_equal(_bits(got), _bits(outs[0].reshape(-1))))))
         # dhopm3 over NCCL equals the in-process oracle run
         hshape = (world * 4, 10, 9)
         vals = np.random.default_rng(7).standard_normal(hshape)

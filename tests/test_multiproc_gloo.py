@@ -16,7 +16,10 @@ import torch.multiprocessing as mp
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-CASES = [("f64", 10), ("f32", 7), ("f16f32", 11), ("bf16f32", 13), ("f32f64", 5), ("f64", 1)]
+# small buffers take the all-gather + local fold path, the last two (> 1 MB
+# over the group) the all-to-all + fold + all-gather path
+CASES = [("f64", 10), ("f32", 7), ("f16f32", 11), ("bf16f32", 13), ("f32f64", 5), ("f64", 1),
+         ("f64", 70001), ("bf16f32", 300001)]
 
 
 def _free_port() -> int:
@@ -40,11 +43,14 @@ def _worker(rank, world, port, q):
 
         names = {torch.float64: "f64", torch.float32: "f32", torch.float16: "f16f32", torch.uint16: "bf16f32"}
 
-        def host_fold(recv, stride, p, n, dst, *, mixed, mode, start):
+        def host_fold(recv, stride, p, n, dst, *, mixed, mode, start, chunk=0):
             name = mode.name if mode is not None else names[dst.dtype]
             arr = recv.numpy()
             contribs = [arr[r * stride: r * stride + n] for r in range(p)]
-            out = O.fold_chunk(contribs, start, name, mixed)
+            if chunk:  # whole buffers: the reference's full ring fold
+                out = O.fold_mixed(contribs, name) if mixed else O.fold_exact(contribs)
+            else:
+                out = O.fold_chunk(contribs, start, name, mixed)
             dst.view(torch.int16 if dst.dtype == torch.uint16 else dst.dtype).copy_(
                 torch.from_numpy(out.view(np.int16) if out.dtype == np.uint16 else out))
 
