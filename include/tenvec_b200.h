@@ -129,6 +129,12 @@ int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64
 int tv_fill(void* A, int dtype, int kind, uint64_t seed, const int64_t* ext, int d, int s,
             int64_t s_lo, int64_t s_hi, void* stream);
 
+/* y <- demote(alpha * promote(x) + beta * promote(y)) elementwise over n
+ * storage elements (kernels.py:191-231 axpby): each product and the sum are
+ * rounded separately in the compute type; beta == 0 never reads y. */
+int tv_axpby(double alpha, const void* x, double beta, void* y, int storage, int compute,
+             int64_t n, void* stream);
+
 /* Read-only streaming probe over `bytes` (16-byte aligned) of device memory:
  * the HBM read roofline the TVC kernels are measured against in bench.py.
  * `sink` is a device uint32 that is written only in a practically impossible

@@ -636,7 +636,6 @@ static unsigned grid_for(int64_t work_items, int64_t per_block, int waves_cap) {
   return (unsigned)need;
 }
 
-static int64_t waste_of(int64_t n, int G) { return cdiv(n, G) * G - n; }
 
 // Lanes per row (units = 16-byte vectors).  A warp load costs one L1
 // wavefront per 128-byte line it touches, so each row segment should be

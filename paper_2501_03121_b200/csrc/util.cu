@@ -233,6 +233,40 @@ __global__ void k_fill(typename St<SD>::T* __restrict__ A, int64_t total, int ki
   }
 }
 
+// --------------------------------------------------------------- axpby ----
+// y = demote(alpha * promote(x) [+ beta * promote(y)]), each product and the
+// sum rounded separately in the compute type (kernels.py:191-231: the pure
+// path's y *= be; y += al * x and the mixed path's cached block give the same
+// value); beta == 0 never reads y.  16-byte vectors when both are aligned.
+template <int SD, typename C>
+__global__ void __launch_bounds__(256)
+    k_axpby(typename St<SD>::T* __restrict__ y, const typename St<SD>::T* __restrict__ x, int64_t n,
+            C alpha, C beta, int has_beta, int vec_ok) {
+  using T = typename St<SD>::T;
+  constexpr int VEC = VecN<SD>::N;
+  auto one = [&](T xv, T yv) -> T {
+    C r = mul_rn(alpha, promote<SD, C>(xv));
+    if (has_beta) r = add_rn(r, mul_rn(beta, promote<SD, C>(yv)));
+    return demote<SD, C>(r);
+  };
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec_ok) {
+    const int64_t nv = n / VEC;
+    for (int64_t q = i; q < nv; q += stride) {
+      Pack16<SD> px, py;
+      px.u = ld_stream16(x + q * VEC);
+      if (has_beta) py.u = *reinterpret_cast<const uint4*>(y + q * VEC);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) py.e[e] = one(px.e[e], has_beta ? py.e[e] : T(0));
+      *reinterpret_cast<uint4*>(y + q * VEC) = py.u;
+    }
+    for (int64_t e = nv * VEC + i; e < n; e += stride) y[e] = one(x[e], has_beta ? y[e] : T(0));
+  } else {
+    for (int64_t e = i; e < n; e += stride) y[e] = one(x[e], has_beta ? y[e] : T(0));
+  }
+}
+
 // --------------------------------------------------------- read stream ----
 // read-only HBM roofline probe: the same 16-byte streaming loads as the TVC
 // kernels, nothing written (the result word is stored only if the XOR of the
@@ -263,6 +297,29 @@ __global__ void __launch_bounds__(256) k_read_stream(const uint4* __restrict__ p
 }  // namespace tv
 
 // ================================================================ C-ABI ====
+extern "C" int tv_axpby(double alpha, const void* x, double beta, void* y, int storage,
+                        int compute, int64_t n, void* stream) {
+  using namespace tv;
+  if (n < 0) return set_error(TV_EKERNEL, "tv_axpby: negative length");
+  if (n == 0) return TV_OK;
+  if (!x || !y) return set_error(TV_EKERNEL, "tv_axpby: null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int vec_ok = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  const int hb = beta != 0.0;
+  int64_t blocks = (n / 4 + 255) / 256;
+  blocks = blocks < 1 ? 1 : (blocks > 148LL * 32 ? 148LL * 32 : blocks);
+  const unsigned g = (unsigned)blocks;
+  switch (mode_id(storage, compute)) {
+    case MODE_F64: k_axpby<TV_F64, double><<<g, 256, 0, st>>>((double*)y, (const double*)x, n, alpha, beta, hb, vec_ok); break;
+    case MODE_F32: k_axpby<TV_F32, float><<<g, 256, 0, st>>>((float*)y, (const float*)x, n, (float)alpha, (float)beta, hb, vec_ok); break;
+    case MODE_F32F64: k_axpby<TV_F32, double><<<g, 256, 0, st>>>((float*)y, (const float*)x, n, alpha, beta, hb, vec_ok); break;
+    case MODE_F16F32: k_axpby<TV_F16, float><<<g, 256, 0, st>>>((uint16_t*)y, (const uint16_t*)x, n, (float)alpha, (float)beta, hb, vec_ok); break;
+    case MODE_BF16F32: k_axpby<TV_BF16, float><<<g, 256, 0, st>>>((uint16_t*)y, (const uint16_t*)x, n, (float)alpha, (float)beta, hb, vec_ok); break;
+    default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
+  }
+  return check_launch("tv_axpby");
+}
+
 extern "C" int tv_read_stream(const void* buf, int64_t bytes, void* sink, void* stream) {
   using namespace tv;
   if (!buf || !sink || bytes < 16 || (reinterpret_cast<uintptr_t>(buf) & 15))

@@ -26,7 +26,7 @@ from .tensor import Shape, Tensor, matricize_dims
 
 __all__ = [
     "MATVEC", "VECMAT", "KernelError", "NormalizationError", "KernelCounters", "task_ranges",
-    "getvc", "tvc_native", "tvc_looped_oracle", "norm2", "normalize", "tvc_regime",
+    "getvc", "tvc_native", "tvc_looped_oracle", "norm2", "normalize", "tvc_regime", "axpby",
 ]
 
 MATVEC = "matvec"
@@ -197,6 +197,37 @@ def tvc_looped_oracle(t: Tensor, x, k: int) -> np.ndarray:
                                 x64.data_ptr(), 1.0, 0.0, y.data_ptr(), _lib.stream_ptr()),
                "tvc_looped_oracle")
     return y.cpu().numpy().reshape(t.shape.drop(k).extents)
+
+
+def axpby(
+    alpha: float,
+    x,
+    beta: float,
+    y,
+    *,
+    mode: PrecisionMode = F64,
+    vl: int = 8,
+    counters: KernelCounters | None = None,
+) -> None:
+    """y := demote(alpha * promote(x) + beta * promote(y)) elementwise, in
+    place (kernels.py:191-231).  ``vl`` sized the reference's cache block and
+    does not change results; beta = 0 never reads y.  Host numpy y is updated
+    in place too."""
+    if tuple(x.shape) != tuple(y.shape) or len(tuple(x.shape)) != 1:
+        raise KernelError("axpby expects two 1-D vectors of equal length")
+    host = None if isinstance(y, torch.Tensor) else y
+    xv = _vec(x, mode, "x")
+    yv = _vec(y, mode, "y")
+    if isinstance(y, torch.Tensor) and yv.data_ptr() != y.data_ptr():
+        raise KernelError("axpby works in place: pass a contiguous CUDA vector")
+    lib = _lib.load()
+    _lib.check(lib.tv_axpby(float(alpha), xv.data_ptr(), float(beta), yv.data_ptr(), mode.tv_storage,
+                            mode.tv_compute, yv.numel(), _lib.stream_ptr()), "axpby")
+    if host is not None:
+        host[...] = yv.cpu().numpy()
+    if counters is not None:
+        n = yv.numel()
+        counters.count("axpby", n + (n if beta != 0.0 else 0), n, mode.storage_bytes)
 
 
 # -- normalisation ----------------------------------------------------------

@@ -102,6 +102,54 @@ def main() -> None:
     out["n"] = np.array(c)
     np.savez_compressed(HERE / "tvc_modes.npz", **out)
 
+    # -- CLI / harness CSV under --deterministic (cli.py, bench.py:330-394) --
+    import contextlib
+    import io
+    import json
+    from tenvec.cli import main as ref_cli
+    cli_cases = [
+        ["tvc", "--dims", "6,7,8", "--mode", "1", "--deterministic", "--iters", "2"],
+        ["tvc", "--dims", "desk:d3", "--mode", "2", "--precision", "bf16f32", "--deterministic"],
+        ["tvc", "--dims", "13^3", "--mode", "0", "--fill", "ramp", "--deterministic"],
+        ["dtvc", "--dims", "8,6,10", "--mode", "0", "--split", "0", "--workers", "3", "--deterministic"],
+        ["dtvc", "--dims", "8,6,10", "--mode", "1", "--split", "0", "--workers", "3",
+         "--assembly", "interleave", "--deterministic"],
+        ["dtvc", "--dims", "8,6,10", "--mode", "2", "--split", "2", "--workers", "4", "--defer",
+         "--deterministic"],
+        ["dtvc", "--dims", "9,5,6", "--mode", "0", "--split", "0", "--workers", "2",
+         "--precision", "f16f32", "--deterministic"],
+        ["hopm", "--dims", "6^4", "--split", "1", "--workers", "2", "--sweeps", "2", "--deterministic"],
+        ["hopm", "--dims", "8^3", "--split", "0", "--workers", "2", "--classical-hopm", "--deterministic"],
+        ["hopm", "--dims", "8^3", "--split", "2", "--workers", "3", "--precision", "f32f64",
+         "--deterministic"],
+        ["triad", "--dims", "1000", "--deterministic"],
+        ["tvc", "--dims", "4^3", "--mode", "5", "--deterministic"],
+        ["dtvc", "--dims", "4^3", "--mode", "0", "--split", "0", "--workers", "9", "--deterministic"],
+    ]
+    records = []
+    for argv in cli_cases:
+        buf, err = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(buf), contextlib.redirect_stderr(err):
+            rc = ref_cli(argv)
+        records.append({"argv": argv, "rc": rc, "stdout": buf.getvalue()})
+    (HERE / "cli.json").write_text(json.dumps(records, indent=1) + "\n")
+
+    # -- axpby (kernels.py:191-231; test_kernels.py:184-210) ------------------
+    rng = np.random.default_rng(31)
+    out = {}
+    for name in sorted(T.MODES):
+        mode = T.MODES[name]
+        x = T.demote(rng.standard_normal(1000), mode).copy()
+        y0 = T.demote(rng.standard_normal(1000), mode).copy()
+        for tag, (alpha, beta) in (("ab", (1.25, -0.5)), ("a0", (2.0, 0.0))):
+            y = y0.copy()
+            T.axpby(alpha, x, beta, y, mode=mode, vl=8)
+            out[f"{name}_{tag}_x"] = x
+            out[f"{name}_{tag}_y0"] = y0
+            out[f"{name}_{tag}_y"] = y
+            out[f"{name}_{tag}_ab"] = np.array([alpha, beta])
+    np.savez_compressed(HERE / "axpby.npz", **out)
+
     # -- ring folds (comm.py:84-134) ----------------------------------------
     rng = np.random.default_rng(31)
     out = {}

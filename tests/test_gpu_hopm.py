@@ -32,6 +32,27 @@ def test_device_conversions_match_reference_bits(tv):
     assert tv.bf16_bits_to_f32(np.array([0x4049], np.uint16))[0] == np.float32(3.140625)
 
 
+@pytest.mark.parametrize("name", ["f64", "f32", "f32f64", "f16f32", "bf16f32"])
+def test_axpby_bitwise_against_reference(tv, name):
+    g = load_golden("axpby")
+    mode = tv.MODES[name]
+    for tag in ("ab", "a0"):
+        alpha, beta = (float(v) for v in g[f"{name}_{tag}_ab"])
+        y = torch.from_numpy(g[f"{name}_{tag}_y0"].copy()).cuda()
+        kc = tv.KernelCounters()
+        tv.axpby(alpha, g[f"{name}_{tag}_x"], beta, y, mode=mode, counters=kc)
+        assert np.array_equal(_bits(y.cpu().numpy()), _bits(g[f"{name}_{tag}_y"])), (name, tag)
+        assert (kc.elements_read, kc.elements_written) == ((2000 if beta else 1000), 1000)
+    # beta = 0 never reads y; misaligned views take the scalar path
+    y = torch.full((1001,), float("nan"), dtype=torch.float64, device="cuda")
+    x = torch.arange(1002, dtype=torch.float64, device="cuda")
+    tv.axpby(2.0, x[1:], 0.0, y)
+    assert torch.equal(y, 2.0 * x[1:])
+    with pytest.raises(tv.KernelError):
+        tv.axpby(1.0, torch.ones(3, dtype=torch.float64, device="cuda"), 1.0,
+                 torch.ones(4, dtype=torch.float64, device="cuda"))
+
+
 def test_normalize_examples(tv):
     x = torch.tensor([3.0, 4.0], dtype=torch.float64, device="cuda")
     assert tv.norm2(x) == 5.0
