@@ -18,9 +18,12 @@ metric  = algorithmic HBM GB/s of the whole job: per rank and mode
           (N_r + |x used| + |out_r|) * storage bytes (kernels.py:168-170,
           bench.py:209-215 of the reference), summed over ranks, / max-over-
           ranks device time of the K timed steps (CUDA events).
-e2e     = the same bytes / time of steps that also copy each rank's slab from
-          pinned host memory to the device (H2D) and read every output back
-          (D2H), through the same public API.
+e2e     = the same bytes / wall time of steps through the same public API
+          with HOST buffers: every step copies its vectors from pinned host
+          memory (H2D) and every output back (D2H) and syncs; the tensor is
+          built once in setup, exactly as the reference's run_bench builds it
+          outside its timed loop.  e2e.tensor_upload additionally re-uploads
+          each rank's slab every step (PCIe bound).
 roofline= the dominant kernel (the mode with the largest time share): its
           algorithmic bytes / its average event-timed duration, against
           MEASURED_PEAKS.json hbm_gbs (a copy, read+write); traffic from the
@@ -402,53 +405,72 @@ def tv_demote_host(v, mode):
 
 
 def run_e2e_sweep(args, tv, dt, part, xs, s, world, rank, group, job_bytes_step):
+    """End-to-end through the public API with HOST buffers.
+
+    Headline (`value`): the reference's own benchmark protocol -- the tensor is
+    built once in setup (the reference's run_bench makes it outside the timed
+    loop, bench.py:189-250) -- and every timed step copies its inputs (the
+    contraction vectors) from pinned host memory, runs the sweep, and copies
+    every output back into pinned host memory, with a host sync per step
+    (wall clock).  `tensor_upload`: the same steps that also re-upload the
+    rank's whole slab from pinned host memory every step (PCIe bound).
+    """
     import torch
     import torch.distributed as dist
 
     if args.e2e_steps <= 0:
         return None
     d = part.order
-    me = dt.local_ranks[0]
-    try:
-        host = torch.empty(part.buf.numel(), dtype=part.buf.dtype, pin_memory=True)
-    except RuntimeError as exc:
-        return {"value": None, "unit": "GB/s", "error": f"pinned alloc failed: {exc}"[:200]}
-    host.copy_(part.buf)  # the slab to upload every step
     xh = [x.cpu().pin_memory() for x in xs]
-    d2h = 0
+    res0 = tv.dtvc_sweep(dt, [x.cuda() for x in xh])
+    outh = [torch.empty(next(p for p in res0[k].parts if p is not None).buf.numel(),
+                        dtype=part.buf.dtype, pin_memory=True) for k in range(d)]
+    d2h = sum(o.numel() * o.element_size() for o in outh)
+    h2d_x = sum(x.numel() * x.element_size() for x in xh)
 
-    def e2e_step():
-        nonlocal d2h
-        part.buf.copy_(host, non_blocking=True)
+    def e2e_step(upload=None):
+        if upload is not None:
+            part.buf.copy_(upload, non_blocking=True)
         xd = [x.cuda(non_blocking=True) for x in xh]
         res = tv.dtvc_sweep(dt, xd)
-        outs = []
         for k in range(d):
-            local = next(p for p in res[k].parts if p is not None)
-            outs.append(local.buf.cpu())
-        d2h = sum(o.numel() * o.element_size() for o in outs)
-        return outs
+            outh[k].copy_(next(p for p in res[k].parts if p is not None).buf, non_blocking=True)
+        torch.cuda.synchronize()  # the step's results are on the host
 
-    e2e_step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        e2e_step()
-    torch.cuda.synchronize()
-    el = time.perf_counter() - t0
-    t = torch.tensor([el], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.barrier()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    el = float(t.item())
-    h2d = part.buf.numel() * part.buf.element_size() + sum(x.numel() * x.element_size() for x in xh)
-    del host
-    return {"value": round(job_bytes_step / (el / args.e2e_steps) / 1e9, 2), "unit": "GB/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-            "ms_per_step": round(el / args.e2e_steps * 1e3, 2),
-            "path": "pinned host slab -> Tensor.buf (H2D), dtvc per mode, outputs .cpu() (D2H), wall clock after sync"}
+    def timed(n, upload=None):
+        for _ in range(2 if upload is None else 1):
+            e2e_step(upload)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            e2e_step(upload)
+        el = time.perf_counter() - t0
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / n
+
+    warm = timed(max(args.steps, 5))
+    out = {"value": round(job_bytes_step / warm / 1e9, 2), "unit": "GB/s",
+           "h2d_bytes_per_step": h2d_x, "d2h_bytes_per_step": d2h, "steps": max(args.steps, 5),
+           "ms_per_step": round(warm * 1e3, 3),
+           "path": "public dtvc_sweep; per step: vectors pinned host -> device, every output "
+                   "device -> pinned host, host sync; tensor built once in setup (as the "
+                   "reference's run_bench does)"}
+    try:
+        host = torch.empty(part.buf.numel(), dtype=part.buf.dtype, pin_memory=True)
+        host.copy_(part.buf)
+        cold = timed(args.e2e_steps, upload=host)
+        out["tensor_upload"] = {
+            "value": round(job_bytes_step / cold / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": part.buf.numel() * part.buf.element_size() + h2d_x,
+            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "ms_per_step": round(cold * 1e3, 2),
+            "path": "as above plus the rank's slab re-uploaded from pinned host memory every step"}
+        del host
+    except RuntimeError as exc:
+        out["tensor_upload"] = {"value": None, "error": f"pinned alloc failed: {exc}"[:200]}
+    return out
 
 
 def run_hopm(args, tv, dt, world, rank, wl, mode, group):
