@@ -384,6 +384,108 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------------- FLAT ----
+// Narrow aligned slabs (vv = v / VEC in [1, 31] 16-byte vectors per row, odd
+// part P of vv in {1, 3, 5, 7}): a warp streams its slab as one flat run of
+// nk * vv vectors, lane l reading vector w = l + 32 t at step t -- every warp
+// load is 512 contiguous bytes and no lane idles (SLABS leaves 32 mod vv
+// lanes idle, 25 % for the C3 / C4 widths).  Lane l's vectors cycle through P
+// columns, (l + 32 t) mod vv, so it keeps P accumulator vectors (slot t mod
+// P); a fixed-order shared-memory fold over the 32 / gcd(32, vv) lanes that
+// visited a column finishes the slab.  Row / column advance incrementally
+// (no division in the stream).
+__host__ __device__ __forceinline__ int gcd_small(int a, int b) {
+  while (b) {
+    const int t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+template <int SD, typename C, int P, int K>
+__global__ void __launch_bounds__(kThreads)
+    k_flat(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+           typename St<SD>::T* __restrict__ y, int64_t u, int nk, int v, C alpha, C beta,
+           int has_beta) {
+  constexpr int VEC = VecN<SD>::N;
+  constexpr int B = P * K;  // steps per batch (a multiple of P: slots are compile-time)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* xs = reinterpret_cast<C*>(smem_raw);
+  C(*red)[32][P][VEC] = reinterpret_cast<C(*)[32][P][VEC]>(
+      smem_raw + ((nk * (int)sizeof(C) + 15) / 16) * 16);
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) xs[i] = promote<SD, C>(x[i]);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int vv = v / VEC;
+  const int L = nk * vv;               // vectors per slab
+  const int q32 = 32 / vv, r32 = 32 % vv;
+  const int64_t warps_total = (int64_t)gridDim.x * kWarps;
+  for (int64_t i = (int64_t)blockIdx.x * kWarps + w; i < u; i += warps_total) {
+    const uint4* base = reinterpret_cast<const uint4*>(A + i * (int64_t)nk * v);
+    C acc[P][VEC];
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[p][e] = C(0);
+    int row = lane / vv, col = lane - (lane / vv) * vv;  // of vector w = lane
+    int wv = lane;
+    for (int t0 = 0; t0 * 32 < L; t0 += B) {
+      uint4 buf[B];
+#pragma unroll
+      for (int tt = 0; tt < B; ++tt) {
+        const int wi = wv + 32 * tt;
+        buf[tt] = ld_stream16(base + (wi < L ? wi : L - 1));  // clamped: no predicate
+      }
+#pragma unroll
+      for (int tt = 0; tt < B; ++tt) {
+        if (wv < L) {
+          C a[VEC];
+          unpack<SD, C>(buf[tt], a);
+          const C xr = xs[row];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[tt % P][e] = fma(a[e], xr, acc[tt % P][e]);
+        }
+        wv += 32;
+        col += r32;
+        row += q32;
+        if (col >= vv) {
+          col -= vv;
+          ++row;
+        }
+      }
+    }
+    // lane l visits each of the P columns congruent to l mod g = gcd(32, vv)
+    // exactly once, so column c gathers the 32 / g lanes l = c mod g + m g:
+    // store slot p of lane l at (c = (l + 32 p) mod vv, m = l / g) and fold
+    // m = 0, 1, ... in order (red is [32 / g][vv] slots of VEC, 32 P in all)
+    const int g = gcd_small(32, vv);
+    C(*slot)[VEC] = reinterpret_cast<C(*)[VEC]>(&red[w][0][0][0]);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int c = (lane + 32 * p) % vv;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) slot[(lane / g) * vv + c][e] = acc[p][e];
+    }
+    __syncwarp();
+    if (lane < vv) {
+      C s[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) s[e] = slot[lane][e];
+      for (int m = 1; m < 32 / g; ++m)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) s[e] += slot[m * vv + lane][e];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const int64_t o = i * v + (int64_t)lane * VEC + e;
+        y[o] = epilogue<SD, C>(s[e], alpha, beta, has_beta != 0, y + o);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // --------------------------------------------------------------- SLABS ----
 // one warp per slab; `units` = v / VEC (aligned) or v (unaligned) in [1, 31];
 // lanes (r = lane / units, c = lane % units), R = 32 / units rows per step.
@@ -676,6 +778,15 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   const bool al_rows = base_al && su_al && nk % VEC == 0;
   const bool al_cols = base_al && su_al && (sk * sb) % 16 == 0 && v % VEC == 0;
   const bool stageable = base_al && contiguous && u > 1 && nk * v * sb <= kStageBytes;
+  // FLAT: aligned narrow contiguous slabs whose width's odd part is 1 or 3
+  // and gcd(32, width) >= 2 (C3 / C4 widths 24, 12, 6 vectors; width 3 folds
+  // 32 lanes per column and measured slower than SLABS), slabs of at least
+  // one warp load
+  const int64_t vvu = v / VEC;
+  const int gg = vvu > 0 ? gcd_small(32, (int)std::min<int64_t>(vvu, 32)) : 1;
+  const int64_t oddp = vvu / gg;
+  const bool flat_ok = al_cols && contiguous && vvu >= 1 && vvu < 32 && (oddp == 1 || oddp == 3) &&
+                       gg >= 2 && nk * vvu >= 32 && nk < (1LL << 24);
   // TENVEC_B200_FORCE=<regime number> pins a regime wherever it is valid
   // (kernel A/B measurements); anything else falls through to the heuristics
   static const int forced = [] {
@@ -688,7 +799,7 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
                     (forced == REG_ROWS_U && v == 1) || (forced == REG_COLS && v > 1 && al_cols) ||
                     (forced == REG_SLABS && v > 1 && al_cols && v / VEC < 32) ||
                     (forced == REG_COLS_U && v > 1) || (forced == REG_SLABS_U && v > 1 && v < 32) ||
-                    (forced == REG_STAGED && stageable);
+                    (forced == REG_STAGED && stageable) || (forced == REG_FLAT && flat_ok);
     if (ok) return forced;
   }
   // measured on B200 (profiles/r01_regime_ab.txt): aligned views always stream
@@ -705,7 +816,7 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // small aligned slabs with short columns (n_k <= 32) leave COLS/SLABS warps
   // too little work per slab: staged tiles win there (paper d = 9, 10 tensors)
   if (al_cols && stageable && nk <= 32 && nk * v * sb <= kStageBytes / 2) return REG_STAGED;
-  if (al_cols) return (v / VEC >= 32) ? REG_COLS : REG_SLABS;
+  if (al_cols) return (v / VEC >= 32) ? REG_COLS : (flat_ok ? REG_FLAT : REG_SLABS);
   if (stageable && nk * v * sb <= kStageBytes / 2) return REG_STAGED;
   return v >= 32 ? REG_COLS_U : REG_SLABS_U;
 }
@@ -856,6 +967,22 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
     case REG_COLS_U:
       rc = launch_cols<SD, C, false>(A, x, y, u, nk, v, su, sk, al, be, hb, st);
       break;
+    case REG_FLAT: {
+      const int vv = (int)(v / VEC);
+      const int P = vv / gcd_small(32, vv);
+      const size_t smem = (size_t)cdiv(nk * (int64_t)sizeof(C), 16) * 16 +
+                          (size_t)kWarps * 32 * P * VEC * sizeof(C);
+      const unsigned grid = grid_for(u, kWarps, 32);
+      auto go = [&](auto kern) {
+        if (smem > 48 * 1024)
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, al,
+                                           be, hb);
+      };
+      if (P == 1) go(k_flat<SD, C, 1, 8>);
+      else go(k_flat<SD, C, 3, 2>);
+      break;
+    }
     case REG_SLABS: {
       const unsigned grid = grid_for(u, kWarps, 32);
       k_slabs<SD, C, 4, true><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk,

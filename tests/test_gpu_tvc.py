@@ -106,9 +106,12 @@ REGIME_CASES = [
     ((7, 40, 256), 1, "cols"),
     ((96, 96, 12), 1, "slabs"),
     ((33, 17, 48), 1, "staged"),
-    ((33, 40, 48), 1, "slabs"),
+    ((33, 40, 48), 1, "flat"),
     ((33, 17, 9), 1, "staged"),
-    ((3, 200, 48), 1, "slabs"),
+    ((3, 200, 48), 1, "flat"),
+    ((5, 100, 32), 1, "flat"),
+    ((7, 41, 96), 1, "flat"),
+    ((3, 200, 20), 1, "slabs"),
     ((4, 300, 21), 1, "slabs_u"),
     ((5, 7, 3), 1, "staged"),
     ((9, 13), 1, "staged"),

@@ -179,7 +179,8 @@ def test_library_argument_validation_without_gpu():
     assert lib.tv_tvc_regime(p, 1, 1000, 96, 12) == 4      # small aligned slabs
     assert lib.tv_tvc_regime(p, 1, 1000, 13, 1) == 8       # unaligned short rows -> staged
     assert lib.tv_tvc_regime(p, 0, 1000, 13, 13) == 8      # unaligned small slabs -> staged
-    assert lib.tv_tvc_regime(p, 1, 1000, 200, 48) == 4     # narrow slabs
+    assert lib.tv_tvc_regime(p, 1, 1000, 200, 48) == 9     # width 12 vectors -> flat
+    assert lib.tv_tvc_regime(p, 1, 1000, 200, 20) == 4     # width 5 -> slabs
     assert lib.tv_tvc_regime(p + 4, 1, 1000, 96, 12) == 7  # misaligned -> scalar slabs
     assert lib.tv_tvc_regime(p, 0, 1000, 13, 1) == 8       # odd fp64 rows -> staged
     assert lib.tv_tvc_regime(p, 0, 1000, 131, 1) == 5      # odd fp64 long rows -> scalar rows
