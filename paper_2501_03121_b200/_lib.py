@@ -20,7 +20,8 @@ TV_F64, TV_F32, TV_F16, TV_BF16 = 0, 1, 2, 3
 TV_FILL_ONES, TV_FILL_RAMP, TV_FILL_HASH = 0, 1, 2
 TV_MAX_RANKS = 64
 REGIMES = {0: "naive", 1: "rows", 2: "rows_short", 3: "cols", 4: "slabs", 5: "rows_u", 6: "cols_u",
-           7: "slabs_u", 8: "staged", 9: "flat"}
+           7: "slabs_u", 8: "staged", 9: "flat",
+           10: "flat_rows"}
 
 _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p

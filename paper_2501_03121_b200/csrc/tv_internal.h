@@ -19,7 +19,8 @@ enum {
   REG_COLS_U = 6,
   REG_SLABS_U = 7,
   REG_STAGED = 8,  // small slabs staged through shared memory (cp.async)
-  REG_FLAT = 9     // narrow aligned slabs streamed as flat warp runs
+  REG_FLAT = 9,      // narrow aligned slabs streamed as flat warp runs
+  REG_FLAT_ROWS = 10  // short aligned rows streamed as flat warp runs
 };
 
 // the five valid (storage, compute) pairs of precision.py:81-87

@@ -486,6 +486,69 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ----------------------------------------------------------- FLAT_ROWS ----
+// Short aligned rows (v == 1, nkv 16-byte vectors per row, odd part S of nkv
+// in {1, 3, 5, 7}): the warp streams a block of 32 S vectors (= 32 / g whole
+// rows, g = nkv / S) as S flat 512-byte loads, every lane busy; each lane
+// dots its vector with its x piece, parks the partial in shared memory, and
+// lane r then sums row r's nkv partials in order.  Replaces per-row shuffle
+// trees and the idle lanes of power-of-two lane groups on rows like C3's 3, 6
+// or 12 vectors.  K blocks per batch keep K * S loads in flight per lane.
+template <int SD, typename C, int S, int K>
+__global__ void __launch_bounds__(kThreads)
+    k_flat_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+                typename St<SD>::T* __restrict__ y, int64_t u, int nk, C alpha, C beta,
+                int has_beta) {
+  constexpr int VEC = VecN<SD>::N;
+  __shared__ C xs[32 * 8];  // nk <= 32 vectors of <= 8 elements
+  __shared__ C part[kWarps][K][32 * S];
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) xs[i] = promote<SD, C>(x[i]);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int nkv = nk / VEC;
+  const int rb = 32 * S / nkv;  // rows per block
+  int piece[S];                 // x piece of this lane's vector at step t
+#pragma unroll
+  for (int t = 0; t < S; ++t) piece[t] = (lane + 32 * t) % nkv;
+  const uint4* base = reinterpret_cast<const uint4*>(A);
+  const int64_t total = u * nkv;  // vectors
+  const int64_t nblocks = (u + rb - 1) / rb;
+  const int64_t warps_total = (int64_t)gridDim.x * kWarps;
+  for (int64_t b0 = ((int64_t)blockIdx.x * kWarps + w) * K; b0 < nblocks; b0 += warps_total * K) {
+    uint4 buf[K][S];
+#pragma unroll
+    for (int kb = 0; kb < K; ++kb)
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        const int64_t wv = (b0 + kb) * 32 * S + lane + 32 * t;
+        buf[kb][t] = ld_stream16(base + (wv < total ? wv : total - 1));  // clamped
+      }
+#pragma unroll
+    for (int kb = 0; kb < K; ++kb)
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        C a[VEC];
+        unpack<SD, C>(buf[kb][t], a);
+        C p = a[0] * xs[piece[t] * VEC];
+#pragma unroll
+        for (int e = 1; e < VEC; ++e) p = fma(a[e], xs[piece[t] * VEC + e], p);
+        part[w][kb][lane + 32 * t] = p;
+      }
+    __syncwarp();
+#pragma unroll
+    for (int kb = 0; kb < K; ++kb) {
+      const int64_t row = (b0 + kb) * rb + lane;
+      if (lane < rb && row < u) {
+        C s = part[w][kb][lane * nkv];
+        for (int j = 1; j < nkv; ++j) s += part[w][kb][lane * nkv + j];
+        y[row] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + row);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // --------------------------------------------------------------- SLABS ----
 // one warp per slab; `units` = v / VEC (aligned) or v (unaligned) in [1, 31];
 // lanes (r = lane / units, c = lane % units), R = 32 / units rows per step.
@@ -787,6 +850,11 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   const int64_t oddp = vvu / gg;
   const bool flat_ok = al_cols && contiguous && vvu >= 1 && vvu < 32 && (oddp == 1 || oddp == 3) &&
                        gg >= 2 && nk * vvu >= 32 && nk < (1LL << 24);
+  // FLAT_ROWS: short aligned contiguous rows of <= 32 vectors, odd part <= 7
+  const int64_t nkv = nk / VEC;
+  const int64_t rodd = nkv > 0 ? nkv / gcd_small(32, (int)std::min<int64_t>(nkv, 32)) : 0;
+  const bool flat_rows_ok = v == 1 && al_rows && contiguous && nkv >= 1 && nkv <= 32 &&
+                            (rodd == 1 || rodd == 3 || rodd == 5 || rodd == 7);
   // TENVEC_B200_FORCE=<regime number> pins a regime wherever it is valid
   // (kernel A/B measurements); anything else falls through to the heuristics
   static const int forced = [] {
@@ -799,7 +867,8 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
                     (forced == REG_ROWS_U && v == 1) || (forced == REG_COLS && v > 1 && al_cols) ||
                     (forced == REG_SLABS && v > 1 && al_cols && v / VEC < 32) ||
                     (forced == REG_COLS_U && v > 1) || (forced == REG_SLABS_U && v > 1 && v < 32) ||
-                    (forced == REG_STAGED && stageable) || (forced == REG_FLAT && flat_ok);
+                    (forced == REG_STAGED && stageable) || (forced == REG_FLAT && flat_ok) ||
+                    (forced == REG_FLAT_ROWS && flat_rows_ok);
     if (ok) return forced;
   }
   // measured on B200 (profiles/r01_regime_ab.txt): aligned views always stream
@@ -809,6 +878,11 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // go through STAGED (contiguous cp.async tiles), which beats scalar loads
   // 2-4x there; larger unaligned views use the peeled / scalar forms.
   if (v == 1) {
+    // rows of 3, 5, 6, 7 vectors idle 25-60 % of ROWS' power-of-two lane
+    // groups; streamed flat they measured 6.2-6.35 vs 4.6-5.9 TB/s.  fp64
+    // rows up to 32 vectors too (their shuffle trees cost twice: C4's 48-
+    // element rows 5.8 vs 5.5 TB/s)
+    if (flat_rows_ok && (nkv & (nkv - 1)) != 0 && (nkv <= 8 || sb == 8)) return REG_FLAT_ROWS;
     if (al_rows) return REG_ROWS;
     if (stageable && nk * sb <= kStagedRowBytes) return REG_STAGED;
     return REG_ROWS_U;
@@ -967,6 +1041,23 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
     case REG_COLS_U:
       rc = launch_cols<SD, C, false>(A, x, y, u, nk, v, su, sk, al, be, hb, st);
       break;
+    case REG_FLAT_ROWS: {
+      const int nkv = (int)(nk / VEC);
+      const int S = nkv / gcd_small(32, nkv);
+      const int rb = 32 * S / nkv;
+      const int64_t nblocks = cdiv(u, rb);
+      const T* At = (const T*)A;
+      const T* xt = (const T*)x;
+      T* yt = (T*)y;
+      const int ik = (int)nk;
+      switch (S) {
+        case 1: k_flat_rows<SD, C, 1, 8><<<grid_for(nblocks, kWarps * 8, 32), kThreads, 0, st>>>(At, xt, yt, u, ik, al, be, hb); break;
+        case 3: k_flat_rows<SD, C, 3, 2><<<grid_for(nblocks, kWarps * 2, 32), kThreads, 0, st>>>(At, xt, yt, u, ik, al, be, hb); break;
+        case 5: k_flat_rows<SD, C, 5, 1><<<grid_for(nblocks, kWarps, 32), kThreads, 0, st>>>(At, xt, yt, u, ik, al, be, hb); break;
+        default: k_flat_rows<SD, C, 7, 1><<<grid_for(nblocks, kWarps, 32), kThreads, 0, st>>>(At, xt, yt, u, ik, al, be, hb); break;
+      }
+      break;
+    }
     case REG_FLAT: {
       const int vv = (int)(v / VEC);
       const int P = vv / gcd_small(32, vv);

@@ -99,7 +99,10 @@ REGIME_CASES = [
     ((64, 256), 1, "rows"),
     ((300, 96), 1, "rows"),
     ((300, 160), 1, "rows"),
-    ((96, 96, 12), 2, "rows"),
+    ((96, 96, 12), 2, "flat_rows"),
+    ((700, 20), 1, "flat_rows"),
+    ((333, 28), 1, "flat_rows"),
+    ((77, 24), 1, "flat_rows"),
     ((5000, 8), 1, "rows"),
     ((1, 8), 1, "rows"),
     ((256, 256), 0, "cols"),

@@ -174,7 +174,8 @@ def test_library_argument_validation_without_gpu():
     p = 1 << 20
     assert lib.tv_tvc_regime(p, 1, 1000, 256, 1) == 1      # rows
     assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 1       # aligned short rows stay rows
-    assert lib.tv_tvc_regime(p, 1, 1000, 12, 1) == 1
+    assert lib.tv_tvc_regime(p, 1, 1000, 12, 1) == 10      # 3-vector rows -> flat rows
+    assert lib.tv_tvc_regime(p, 1, 1000, 16, 1) == 1       # 4-vector rows stay rows
     assert lib.tv_tvc_regime(p, 1, 1, 2048, 4096) == 3     # columns
     assert lib.tv_tvc_regime(p, 1, 1000, 96, 12) == 4      # small aligned slabs
     assert lib.tv_tvc_regime(p, 1, 1000, 13, 1) == 8       # unaligned short rows -> staged
