@@ -294,6 +294,47 @@ def test_dhopm3_validation_and_zero_tensor(tv):
         tv.dhopm3(tv.distribute(tv.Tensor.from_array(np.zeros((3, 3, 3))), 0, 2))
 
 
+# stated accuracy of the mixed-precision power method against fp64, max abs
+# factor error and relative lambda error after 3 sweeps (demo 05's setting:
+# the reference itself shows 2.0e-8 / 1.4e-4 / 1.4e-3 for f32f64 / f16f32 /
+# bf16f32 factors and 8.6e-10 / 3.7e-4 / 1.84e-2 for lambda there -- brain
+# storage truncates every stored intermediate, biasing lambda low)
+MIXED_BOUNDS = {"f32f64": (1e-7, 1e-8), "f16f32": (1e-3, 1e-3), "bf16f32": (5e-3, 2.5e-2)}
+
+
+@pytest.mark.parametrize("name", sorted(MIXED_BOUNDS))
+def test_mixed_dhopm3_against_fp64_oracle(tv, name):
+    rng = np.random.default_rng(5)
+    n = 48
+    a64 = rng.integers(1, 98, (n, n, n)).astype(float)
+    x0 = O.initial_vectors((n, n, n), "f64", kind="random", seed=9)
+    ref_v, ref_l = O.dhopm3(a64, 1, 2, [v.copy() for v in x0], 3, "f64")
+    mode = tv.MODES[name]
+    t = tv.Tensor.from_array(a64, mode)
+    start = [O.demote(v.astype(mode.compute_dtype), name).copy() for v in x0]
+    res = tv.dhopm3(tv.distribute(t, 1, 2), start, sweeps=3)
+    vec_tol, lam_tol = MIXED_BOUNDS[name]
+    err = max(float(np.max(np.abs(O.promote(a, name).astype(float) - b)))
+              for a, b in zip(res.vectors, ref_v))
+    assert err <= vec_tol, (name, err)
+    lam_err = abs(res.norms[-1][-1] - ref_l[-1][-1]) / ref_l[-1][-1]
+    assert lam_err <= lam_tol, (name, lam_err)
+
+
+def test_large_bf16_dhopm3_tracks_fp64_on_device(tv):
+    """512^3 hash tensor: the bf16-storage power method (C5's mode) against the
+    fp64 one, both on the device, split over 4 in-process ranks."""
+    shape = tv.Shape((512, 512, 512))
+    res = {}
+    for name in ("f64", "bf16f32"):
+        dt = tv.distribute_generated(shape, 2, 4, tv.MODES[name], fill="hash", seed=3)
+        res[name] = tv.dhopm3(dt, sweeps=5)
+    for a, b in zip(res["bf16f32"].vectors, res["f64"].vectors):
+        assert float(np.max(np.abs(O.promote(a, "bf16f32").astype(float) - b))) <= 5e-3
+    l16, l64 = res["bf16f32"].norms[-1][-1], res["f64"].norms[-1][-1]
+    assert abs(l16 - l64) / l64 <= MIXED_BOUNDS["bf16f32"][1]
+
+
 def test_initial_vectors(tv):
     xs = tv.initial_vectors(tv.Shape((4, 9)))
     assert np.allclose(xs[0], 0.5) and np.allclose(xs[1], 1.0 / 3.0)
