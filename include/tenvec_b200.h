@@ -123,6 +123,12 @@ int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64
                          int64_t chunk, int start, int storage, int compute, int mixed,
                          void* dst, void* stream);
 
+/* dst[e] = srcs[e / chunk][e] (srcs a HOST array of p device pointers, e.g.
+ * peer buffers of a symmetric-memory group): the gather phase of the
+ * peer-memory allreduce, where rank r's buffer holds reduced ring chunk r. */
+int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t chunk, int dtype,
+                   void* dst, void* stream);
+
 /* Fill the rank-local slab [s_lo, s_hi) along mode s of a global tensor with
  * extents ext[0..d-1] (last mode fastest) from the GLOBAL linear index g:
  * ones -> 1, ramp -> (g mod 97) + 1, hash -> (splitmix64(seed, g) mod 97) + 1. */

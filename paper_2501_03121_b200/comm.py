@@ -325,14 +325,27 @@ class RankGroup:
     ``fold`` is the local reduction (default: the tv_rank_fold kernel); CPU
     multi-process tests inject a host fold to exercise the chunk logic over
     gloo without a GPU.
+
+    ``algo`` (default from TENVEC_B200_ALLREDUCE, else "exact"):
+      exact  all-to-all of ring chunks + fold kernel + all-gather (NCCL moves
+             the bytes), reference-exact;
+      p2p    the same fold over PEER memory: every rank's buffer is a
+             symmetric-memory allocation (torch symm_mem, NVLink mapped), rank c
+             folds ring chunk c straight from its peers' buffers with the fold
+             kernel, a select kernel gathers the reduced chunks; three device
+             barriers, no NCCL, reference-exact;
+      nccl   ncclAllReduce (rank-consistent, not reference-ordered).
     """
 
-    def __init__(self, group=None, *, algo: str = "exact", fold: FoldFn | None = None):
+    def __init__(self, group=None, *, algo: str | None = None, fold: FoldFn | None = None):
+        import os
+
         import torch.distributed as dist
 
         if not dist.is_initialized():
             raise CollectiveError("torch.distributed is not initialised")
-        if algo not in ("exact", "nccl"):
+        algo = algo or os.environ.get("TENVEC_B200_ALLREDUCE", "exact")
+        if algo not in ("exact", "nccl", "p2p"):
             raise CollectiveError(f"unknown allreduce algorithm {algo!r}")
         self._dist = dist
         self.group = group
@@ -341,6 +354,45 @@ class RankGroup:
         self.algo = algo
         self.fold = fold or device_fold_strided
         self.counters = [CommCounters() for _ in range(self.size)]
+        self._sym = None  # (uint8 symmetric tensor, handle)
+
+    # -- peer memory (algo="p2p") ---------------------------------------------
+    def _symmetric(self, nbytes: int, device) -> tuple[torch.Tensor, object]:
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if self._sym is None or self._sym[0].numel() < nbytes:
+            name = (self.group or self._dist.group.WORLD).group_name
+            try:
+                symm_mem.enable_symm_mem_for_group(name)
+            except Exception:  # noqa: BLE001 - newer torch enables groups lazily
+                pass
+            cap = max(nbytes, 1 << 20)
+            t = symm_mem.empty(cap, dtype=torch.uint8, device=device)
+            self._sym = (t, symm_mem.rendezvous(t, name))
+        return self._sym
+
+    def _reduce_p2p(self, buf: torch.Tensor, mixed: bool, mode: PrecisionMode | None,
+                    sizes: list[int]) -> None:
+        p, rank = self.size, self.rank
+        n, sb = buf.numel(), buf.element_size()
+        sym, hdl = self._symmetric(n * sb, buf.device)
+        mine = as_bits(sym[: n * sb].view(as_bits(buf).dtype))
+        mine.copy_(as_bits(buf))
+        ptrs = [int(ptr) for ptr in hdl.buffer_ptrs]
+        q = sizes[0]
+        lib = _lib.load()
+        st, ct = _pair_for(buf, mode)
+        stream = _lib.stream_ptr()
+        hdl.barrier(channel=0)                      # every partial is in place
+        if sizes[rank]:
+            off = rank * q * sb
+            srcs = (ctypes.c_void_p * p)(*[ptr + off for ptr in ptrs])
+            _lib.check(lib.tv_rank_fold(srcs, p, sizes[rank], 0, rank, st, ct, int(mixed),
+                                        ptrs[rank] + off, stream), "p2p fold")
+        hdl.barrier(channel=0)                      # every chunk is reduced
+        srcs = (ctypes.c_void_p * p)(*ptrs)
+        _lib.check(lib.tv_rank_select(srcs, p, n, q, st, buf.data_ptr(), stream), "p2p gather")
+        hdl.barrier(channel=0)                      # peers done reading this buffer
 
     def _check_rank(self, rank: int) -> None:
         if rank != self.rank:
@@ -364,6 +416,9 @@ class RankGroup:
             return
         if self.algo == "nccl" and not mixed:
             dist.all_reduce(buf, group=self.group)
+            return
+        if self.algo == "p2p" and n * buf.element_size() * p > SMALL_GATHER_BYTES:
+            self._reduce_p2p(buf, mixed, mode, sizes)
             return
         if n * buf.element_size() * p <= SMALL_GATHER_BYTES:
             # latency-bound sizes (dHOPM3 vectors): one all-gather of every

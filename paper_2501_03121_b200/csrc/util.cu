@@ -206,6 +206,34 @@ static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int sta
   return check_launch("tv_rank_fold");
 }
 
+// -------------------------------------------------------------- select ----
+// dst[e] = srcs[e / chunk][e]: the gather phase of a peer-memory allreduce
+// (rank r's buffer holds the reduced ring chunk r).  16-byte vectors when the
+// chunk length and every pointer allow it.
+template <int SB>
+__global__ void k_select(Srcs srcs, int p, int64_t n, int64_t chunk, unsigned char* __restrict__ dst,
+                         int vec_ok) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec_ok) {
+    constexpr int VE = 16 / SB;  // elements per vector
+    const int64_t nv = n / VE;
+    const int64_t cv = chunk / VE;
+    for (int64_t q = i0; q < nv; q += stride) {
+      const int r = (int)(q / cv);
+      reinterpret_cast<uint4*>(dst)[q] =
+          ld_stream16(reinterpret_cast<const uint4*>(srcs.p[r < p ? r : p - 1]) + q);
+    }
+    return;
+  }
+  for (int64_t e = i0; e < n; e += stride) {
+    const int r = (int)(e / chunk);
+    const unsigned char* s = static_cast<const unsigned char*>(srcs.p[r < p ? r : p - 1]);
+#pragma unroll
+    for (int b = 0; b < SB; ++b) dst[e * SB + b] = s[e * SB + b];
+  }
+}
+
 // ---------------------------------------------------------------- fill ----
 __host__ __device__ inline uint64_t fill_hash(uint64_t seed, uint64_t g) {
   uint64_t z = (g + 1ULL) * 0x9E3779B97F4A7C15ULL + seed * 0xD1B54A32D192ED03ULL;
@@ -392,6 +420,33 @@ extern "C" int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, i
   for (int r = 0; r < p; ++r)
     s.p[r] = static_cast<const char*>(src) + (size_t)r * (size_t)src_stride_elems * (size_t)sb;
   return fold_dispatch(s, p, n, chunk, start, storage, compute, mixed, dst, stream);
+}
+
+extern "C" int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t chunk, int dtype,
+                              void* dst, void* stream) {
+  using namespace tv;
+  if (!srcs || p < 1 || p > TV_MAX_RANKS || n < 0 || chunk < 1 || !dst)
+    return set_error(TV_ECOLL, "tv_rank_select: bad arguments");
+  const int sb = dtype_bytes(dtype);
+  if (sb <= 0) return set_error(TV_EMODE, "tv_rank_select: bad dtype");
+  if (n == 0) return TV_OK;
+  Srcs s{};
+  uintptr_t bits = reinterpret_cast<uintptr_t>(dst);
+  for (int r = 0; r < p; ++r) {
+    if (!srcs[r]) return set_error(TV_ECOLL, "tv_rank_select: null source");
+    s.p[r] = srcs[r];
+    bits |= reinterpret_cast<uintptr_t>(srcs[r]);
+  }
+  const int vec_ok = (bits & 15) == 0 && ((chunk * sb) % 16) == 0 && ((n * sb) % 16) == 0;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned g = grid_1d(vec_ok ? n * sb / 16 : n, 256);
+  unsigned char* d = static_cast<unsigned char*>(dst);
+  switch (sb) {
+    case 8: k_select<8><<<g, 256, 0, st>>>(s, p, n, chunk, d, vec_ok); break;
+    case 4: k_select<4><<<g, 256, 0, st>>>(s, p, n, chunk, d, vec_ok); break;
+    default: k_select<2><<<g, 256, 0, st>>>(s, p, n, chunk, d, vec_ok); break;
+  }
+  return check_launch("tv_rank_select");
 }
 
 extern "C" int tv_fill(void* A, int dtype, int kind, uint64_t seed, const int64_t* ext, int d,

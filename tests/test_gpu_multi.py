@@ -62,15 +62,23 @@ def _worker(rank, world, port, q):
         # a reduction above the small-gather threshold: all-to-all + fold + all-gather
         big = (64, 64, 2 * world, 64)
         fullb = O.fill_values(big, "hash", seed=6).reshape(big)
-        for name in ("f32", "bf16f32"):
+        p2p = tv.RankGroup(algo="p2p")  # the same fold over symmetric (peer) memory
+        for name in ("f32", "bf16f32", "f64"):
             mode = tv.MODES[name]
             hostb = O.demote(fullb.reshape(-1), name).reshape(big)
-            dt = tv.distribute_generated(tv.Shape(big), 2, world, mode, fill="hash", seed=6, group=group)
             x = O.demote((np.arange(big[2]) % 3) + 1.0, name).copy()
             parts, ranges = O.split(hostb, 2, world)
             _, outs, _ = O.dtvc(parts, ranges, 2, x, 2, name)
-            got = tv.dtvc(dt, x, 2).parts[0].to_numpy()
-            ok.append((name, "big-reduce", 2, bool(np.array_equal(_bits(got), _bits(outs[0].reshape(-1))))))
+            for tag, grp in (("exact", group), ("p2p", p2p)):
+                dt = tv.distribute_generated(tv.Shape(big), 2, world, mode, fill="hash", seed=6, group=grp)
+                for _ in range(2):  # twice: the symmetric buffer is reused
+                    got = tv.dtvc(dt, x, 2).parts[0].to_numpy()
+                ok.append((name, "big-reduce", tag, bool(np.array_equal(_bits(got), _bits(outs[0].reshape(-1))))))
+        # ragged reduction (n not a multiple of p or of 16 bytes) over peer memory
+        rag = torch.arange(1, 300_003, dtype=torch.float32, device="cuda") * (rank + 1)
+        want = torch.arange(1, 300_003, dtype=torch.float32) * sum(r + 1 for r in range(world))
+        p2p.all_reduce_sum(rank, rag)
+        ok.append(("f32", "ragged-p2p", 0, bool(torch.equal(rag.cpu(), want))))
         # dhopm3 over NCCL equals the in-process oracle run
         hshape = (world * 4, 10, 9)
         vals = np.random.default_rng(7).standard_normal(hshape)
