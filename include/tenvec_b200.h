@@ -79,9 +79,16 @@ int tv_tvc_naive(const void* A, int storage, int compute, int64_t u, int64_t nk,
 
 /* Which kernel regime tv_tvc would pick for this view: 1 rows, 2 short rows,
  * 3 columns, 4 narrow slabs, and their unaligned (scalar-load) forms 5 rows,
- * 6 columns, 7 slabs, 8 small slabs staged through shared memory (0 is the
- * naive kernel, tv_tvc_naive only); -1 on invalid arguments. */
+ * 6 columns, 7 slabs, 8 slabs staged through shared memory by TMA bulk
+ * copies, 9 flat narrow slabs, 10 flat short rows (0 is the naive kernel,
+ * tv_tvc_naive only); -1 on invalid arguments. */
 int tv_tvc_regime(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
+
+/* Diagnostic: pin the regime tv_tvc uses wherever the view can take it
+ * (regime codes as tv_tvc_regime; <= 0 restores the heuristics).  Returns the
+ * previous override (-1 = none).  Initialised from TENVEC_B200_FORCE.  Not in
+ * the reference; used by the regime coverage tests and kernel A/B runs. */
+int tv_set_regime_override(int regime);
 
 /* getvc over an m x n row-major view with leading dimension lda >= n.
  * trans 0 = matvec (x has n, y has m), 1 = vecmat (x has m, y has n). */

@@ -35,6 +35,7 @@
 // bits.  There are no tensor cores here: arithmetic intensity is 0.25-1 FLOP/B.
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -612,32 +613,77 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // -------------------------------------------------------------- STAGED ----
-// Small slabs (<= kStageBytes / 2), aligned or not: whole-slab tiles of the
-// flat buffer are copied global -> shared with 16-byte cp.async (aligned-down
-// start, zero-filled ragged end), double-buffered per CTA, so HBM sees pure
-// contiguous 512-byte-per-warp streaming whatever n_k and v are; the dot
+// Slabs that fit one tile, aligned or not: whole-slab tiles of the flat
+// buffer are copied global -> shared by ONE TMA bulk copy each (aligned-down
+// 16-byte start; the < 16-byte ragged end of the buffer by scalar loads),
+// double-buffered per CTA on two mbarriers, so HBM sees pure contiguous
+// streaming whatever n_k and v are and the SM issues no load instructions
+// for the tile (the cp.async form was issue-bound at 4.1-5.8 TB/s); the dot
 // products are then read from shared memory.  Output o of a tile = (slab
 // o / v, column o % v); G lanes share an output (j = g, g + G, ...) and
 // combine with an xor shuffle.  For v == 1, G lanes read consecutive words.
-constexpr int kStageBytes = 16384;
-constexpr int kStagedRowBytes = 512;  // v == 1 rows up to this size are staged
+constexpr int kStageBytes = 49152;
+constexpr int kStagedRowBytes = 512;     // aligned v == 1 rows up to this size are staged
+constexpr int kStagedRowBytesU = 2048;  // unaligned ones
+// stage size (bytes per tile buffer); TENVEC_B200_STAGE_BYTES overrides it for A/B runs
+static int stage_bytes() {
+  static const int b = [] {
+    const char* e = getenv("TENVEC_B200_STAGE_BYTES");
+    const int r = e ? atoi(e) : kStageBytes;
+    return r < 4096 ? 4096 : (r > 65536 ? 65536 : r / 16 * 16);
+  }();
+  return b;
+}
+static int stage_count() {  // TENVEC_B200_STAGES: tiles per CTA ring (2..4)
+  static const int n = [] {
+    const char* e = getenv("TENVEC_B200_STAGES");
+    const int r = e ? atoi(e) : 2;
+    return r < 2 ? 2 : (r > 4 ? 4 : r);
+  }();
+  return n;
+}
+static int staged_row_bytes() {
+  static const int b = [] {
+    const char* e = getenv("TENVEC_B200_STAGE_ROW");
+    return e ? atoi(e) : kStagedRowBytesU;
+  }();
+  return b;
+}
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+// TMA 1-D bulk copies completing on an mbarrier (one elected thread issues a
+// whole tile; every thread waits on the barrier's phase)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TV_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TV_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 template <int SD, typename C, bool VROW>
 __global__ void __launch_bounds__(kThreads)
     k_staged(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
              typename St<SD>::T* __restrict__ y, int64_t u, int nk, int v, int spt, int64_t ntiles,
-             int G, C alpha, C beta, int has_beta) {
+             int G, int sbytes, int nst, C alpha, C beta, int has_beta) {
   using T = typename St<SD>::T;
   constexpr int SB = sizeof(T);
   constexpr int VEC = VecN<SD>::N;
@@ -646,24 +692,32 @@ __global__ void __launch_bounds__(kThreads)
   const int xs_pad = (nk * (int)sizeof(C) + 15) / 16 * 16;
   C* xs = reinterpret_cast<C*>(smem_raw);
   unsigned char* const stage0 = smem_raw + xs_pad;
-  auto stage = [&](int k) { return stage0 + (k & 1) * (kStageBytes + 16); };
-  C* red = reinterpret_cast<C*>(smem_raw + xs_pad + 2 * (kStageBytes + 16));
+  auto stage = [&](int k) { return stage0 + k * (sbytes + 16); };
+  C* red = reinterpret_cast<C*>(smem_raw + xs_pad + nst * (sbytes + 16));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + xs_pad + nst * (sbytes + 16) +
+                                               (kThreads * sizeof(C) + 7) / 8 * 8);
   for (int i = threadIdx.x; i < nk; i += blockDim.x) xs[i] = promote<SD, C>(x[i]);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < nst; ++k) mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
   const int L = nk * v;
-  const uintptr_t gbase = reinterpret_cast<uintptr_t>(A);
+  const unsigned char* gbase = reinterpret_cast<const unsigned char*>(A);
   const int64_t total_bytes = u * (int64_t)L * SB;
-  auto issue = [&](int64_t tile, unsigned char* dst) {
+  const int64_t bulk_end = total_bytes & ~(int64_t)15;  // TMA moves whole 16-byte units
+  // tile -> [a0, a1): 16-byte aligned bulk range; the < 16-byte ragged end of
+  // the buffer (last tile only) is copied by scalar loads after the wait
+  auto issue = [&](int64_t tile, int k) {
     const int64_t b0 = tile * spt * (int64_t)L * SB;
     const int64_t s1 = (tile + 1) * spt < u ? (tile + 1) * spt : u;
     const int64_t a0 = b0 & ~(int64_t)15;
-    const int nvec = (int)((s1 * (int64_t)L * SB - a0 + 15) / 16);
-    for (int vi = threadIdx.x; vi < nvec; vi += blockDim.x) {
-      const int64_t off = a0 + (int64_t)vi * 16;
-      const int64_t left = total_bytes - off;
-      cp_async16(dst + vi * 16, reinterpret_cast<const void*>(gbase + off), left >= 16 ? 16 : (int)left);
-    }
-    cp_async_commit();
+    const int64_t e16 = (s1 * (int64_t)L * SB + 15) & ~(int64_t)15;
+    const int64_t a1 = e16 < bulk_end ? e16 : bulk_end;
+    const unsigned nb = a1 > a0 ? (unsigned)(a1 - a0) : 0u;
+    mbar_expect_tx(&bars[k], nb);
+    if (nb) bulk_g2s(stage(k), gbase + a0, nb, &bars[k]);
   };
 
   // thread = (gi, oi): output oi of each pass of `per` outputs, j-slice gi of G
@@ -672,27 +726,43 @@ __global__ void __launch_bounds__(kThreads)
   const int oi = threadIdx.x - gi * per;
   // units of a "row" (output's j range): 16-byte chunks when VROW, else elements
   const int nunits = VROW ? nk / VEC : nk;
+  // nst-stage ring: tiles blockIdx.x + i * gridDim.x, i = 0 .. nst - 2, are in
+  // flight before the first wait; stage `cur` holds the current tile
   int64_t tile = blockIdx.x;
-  if (tile < ntiles) issue(tile, stage(0));
-  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
-    const int64_t next = tile + gridDim.x;
-    if (next < ntiles) {
-      issue(next, stage(it + 1));
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nst - 1; ++k)
+      if (tile + k * (int64_t)gridDim.x < ntiles) issue(tile + k * (int64_t)gridDim.x, k);
+  int cur = 0;
+  unsigned phase = 0;
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t ahead = tile + (nst - 1) * (int64_t)gridDim.x;
+    if (threadIdx.x == 0 && ahead < ntiles) {
+      // stage cur - 1 was released by the trailing __syncthreads of the
+      // previous iteration; order those generic-proxy reads before the TMA write
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(ahead, cur == 0 ? nst - 1 : cur - 1);
     }
-    __syncthreads();
+    mbar_wait(&bars[cur], phase);
+    unsigned char* const sp0 = stage(cur);
+    if (tile == ntiles - 1 && (total_bytes & 15)) {  // block-uniform: ragged buffer end
+      const int64_t a0 = (tile * spt * (int64_t)L * SB) & ~(int64_t)15;
+      for (int64_t b = bulk_end + threadIdx.x; b < total_bytes; b += blockDim.x) sp0[b - a0] = gbase[b];
+      __syncthreads();
+    }
+    if (++cur == nst) {
+      cur = 0;
+      phase ^= 1u;
+    }
     const int64_t s0 = tile * spt;
     const int ns = (int)(spt < u - s0 ? spt : u - s0);
-    const T* t = reinterpret_cast<const T*>(stage(it) + ((s0 * (int64_t)L * SB) & 15));
+    const T* t = reinterpret_cast<const T*>(sp0 + ((s0 * (int64_t)L * SB) & 15));
     const int outs = ns * v;
     for (int ob = 0; ob < outs; ob += per) {  // block-uniform trip count
       const int o = ob + oi;
       C acc[NA];
 #pragma unroll
       for (int e = 0; e < NA; ++e) acc[e] = C(0);
-      if (o < outs) {
+      if (o < outs && gi < G) {  // kThreads % G threads idle
         const int s = o / v;
         const int l = o - s * v;
         if constexpr (VROW) {
@@ -832,6 +902,21 @@ static int pick_col_phases(int64_t nk, int64_t stripes, int64_t u) {
   return jr;
 }
 
+// TENVEC_B200_FORCE=<regime number> / tv_set_regime_override pin a regime
+// wherever it is valid (kernel A/B measurements, regime coverage tests)
+static std::atomic<int> g_forced{-2};
+static int forced_regime() {
+  int f = g_forced.load(std::memory_order_relaxed);
+  if (f == -2) {
+    const char* e = getenv("TENVEC_B200_FORCE");
+    int want = e ? atoi(e) : -1;
+    int expect = -2;
+    g_forced.compare_exchange_strong(expect, want);
+    f = g_forced.load(std::memory_order_relaxed);
+  }
+  return f;
+}
+
 static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t v, int64_t su,
                           int64_t sk) {
   const int VEC = 16 / sb;
@@ -840,7 +925,8 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   const bool contiguous = su == nk * v && sk == v;
   const bool al_rows = base_al && su_al && nk % VEC == 0;
   const bool al_cols = base_al && su_al && (sk * sb) % 16 == 0 && v % VEC == 0;
-  const bool stageable = base_al && contiguous && u > 1 && nk * v * sb <= kStageBytes;
+  const int stb = stage_bytes();
+  const bool stageable = base_al && contiguous && u > 1 && nk * v * sb + 16 <= stb;
   // FLAT: aligned narrow contiguous slabs whose width's odd part is 1 or 3
   // and gcd(32, width) >= 2 (C3 / C4 widths 24, 12, 6 vectors; width 3 folds
   // 32 lanes per column and measured slower than SLABS), slabs of at least
@@ -855,12 +941,8 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   const int64_t rodd = nkv > 0 ? nkv / gcd_small(32, (int)std::min<int64_t>(nkv, 32)) : 0;
   const bool flat_rows_ok = v == 1 && al_rows && contiguous && nkv >= 1 && nkv <= 32 &&
                             (rodd == 1 || rodd == 3 || rodd == 5 || rodd == 7);
-  // TENVEC_B200_FORCE=<regime number> pins a regime wherever it is valid
-  // (kernel A/B measurements); anything else falls through to the heuristics
-  static const int forced = [] {
-    const char* e = getenv("TENVEC_B200_FORCE");
-    return e ? atoi(e) : -1;
-  }();
+  // a forced regime the view cannot take falls through to the heuristics
+  const int forced = forced_regime();
   if (forced > 0) {
     const bool ok = (forced == REG_ROWS && v == 1 && al_rows) ||
                     (forced == REG_ROWS_SHORT && v == 1 && al_rows && nk / VEC <= 8) ||
@@ -882,16 +964,19 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
     // groups; streamed flat they measured 6.2-6.35 vs 4.6-5.9 TB/s.  fp64
     // rows up to 32 vectors too (their shuffle trees cost twice: C4's 48-
     // element rows 5.8 vs 5.5 TB/s)
+    // short rows (<= 512 B aligned, <= 2 KB unaligned) stream best as
+    // contiguous TMA tiles: 6.7-6.8 TB/s vs 5.8-6.6 (FLAT_ROWS / ROWS) and
+    // 4.8 (ROWS_U, 175-element fp64 rows)
+    if (stageable && nk * sb <= (al_rows ? kStagedRowBytes : staged_row_bytes())) return REG_STAGED;
     if (flat_rows_ok && (nkv & (nkv - 1)) != 0 && (nkv <= 8 || sb == 8)) return REG_FLAT_ROWS;
     if (al_rows) return REG_ROWS;
-    if (stageable && nk * sb <= kStagedRowBytes) return REG_STAGED;
     return REG_ROWS_U;
   }
   // small aligned slabs with short columns (n_k <= 32) leave COLS/SLABS warps
   // too little work per slab: staged tiles win there (paper d = 9, 10 tensors)
-  if (al_cols && stageable && nk <= 32 && nk * v * sb <= kStageBytes / 2) return REG_STAGED;
+  if (al_cols && stageable && nk <= 32 && nk * v * sb <= stb / 2) return REG_STAGED;
   if (al_cols) return (v / VEC >= 32) ? REG_COLS : (flat_ok ? REG_FLAT : REG_SLABS);
-  if (stageable && nk * v * sb <= kStageBytes / 2) return REG_STAGED;
+  if (stageable) return REG_STAGED;  // any unaligned slab that fits one tile
   return v >= 32 ? REG_COLS_U : REG_SLABS_U;
 }
 
@@ -958,26 +1043,43 @@ static void launch_staged(const void* A, const void* x, void* y, int64_t u, int6
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
   const int64_t slab_bytes = nk * v * (int64_t)sizeof(T);
-  const int spt = (int)std::max<int64_t>(1, std::min<int64_t>(kStageBytes / slab_bytes, u));
-  const int64_t ntiles = cdiv(u, spt);
+  const int sbytes = stage_bytes();
+  // slabs per tile: as many as fit, trimmed so the tile's outputs fill whole
+  // passes of kThreads threads (269 outputs would run a 13-thread 2nd pass)
   const bool vrow = v == 1 && (slab_bytes % 16) == 0;
   const int64_t units = vrow ? nk / VEC : nk;
-  const int64_t outs = (int64_t)spt * v;
-  int G = 1;  // idle threads split each output's j range
-  while (G < 8 && outs * G * 2 <= kThreads && G * 2 <= units) G <<= 1;
-  const size_t smem = (size_t)cdiv(nk * (int64_t)sizeof(C), 16) * 16 + 2 * (kStageBytes + 16) +
-                      kThreads * sizeof(C);
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, 6LL * sm_count());
+  // idle threads split each output's j range (G need not be a power of two)
+  auto g_of = [&](int64_t s) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>({kThreads / (s * v), units / 2, 32}));
+  };
+  auto eff = [&](int64_t s) {  // busy fraction of the thread passes over a tile
+    const int64_t per = kThreads / g_of(s);
+    return (double)(s * v) / (double)(cdiv(s * v, per) * per);
+  };
+  int64_t spt64 = std::max<int64_t>(1, std::min<int64_t>(sbytes / slab_bytes, u));
+  if (spt64 * v >= kThreads) {
+    const int64_t trim = std::max<int64_t>(1, (spt64 * v / kThreads) * kThreads / v);
+    if (eff(trim) > eff(spt64) + 1e-9) spt64 = trim;
+  }
+  const int spt = (int)spt64;
+  const int64_t ntiles = cdiv(u, spt);
+  const int G = g_of(spt64);
+  const int nst = stage_count();
+  const size_t smem = (size_t)cdiv(nk * (int64_t)sizeof(C), 16) * 16 + nst * (sbytes + 16) +
+                      (kThreads * sizeof(C) + 7) / 8 * 8 + nst * sizeof(uint64_t);
+  // persistent grid: as many CTAs as are co-resident, tiles strided over them
+  const int per_sm = std::max(1, std::min(8, (int)(228 * 1024 / (smem + 1024))));
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)per_sm * sm_count());
   if (vrow) {
     auto kern = k_staged<SD, C, true>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, spt,
-                                       ntiles, G, al, be, hb);
+                                       ntiles, G, sbytes, nst, al, be, hb);
   } else {
     auto kern = k_staged<SD, C, false>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, spt,
-                                       ntiles, G, al, be, hb);
+                                       ntiles, G, sbytes, nst, al, be, hb);
   }
 }
 
@@ -1145,6 +1247,12 @@ extern "C" int tv_tvc_naive(const void* A, int storage, int compute, int64_t u, 
 
 extern "C" int tv_tvc_regime(const void* A, int storage, int64_t u, int64_t nk, int64_t v) {
   return tv::regime_of(A, storage, u, nk, v);
+}
+
+extern "C" int tv_set_regime_override(int regime) {
+  const int prev = tv::forced_regime();
+  tv::g_forced.store(regime > 0 ? regime : -1, std::memory_order_relaxed);
+  return prev;
 }
 
 extern "C" int tv_getvc(int trans, const void* A, int storage, int compute, int64_t m, int64_t n,

@@ -173,9 +173,9 @@ def test_library_argument_validation_without_gpu():
     # regime choice is host logic: aligned fake pointers, no dereference
     p = 1 << 20
     assert lib.tv_tvc_regime(p, 1, 1000, 256, 1) == 1      # rows
-    assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 1       # aligned short rows stay rows
-    assert lib.tv_tvc_regime(p, 1, 1000, 12, 1) == 10      # 3-vector rows -> flat rows
-    assert lib.tv_tvc_regime(p, 1, 1000, 16, 1) == 1       # 4-vector rows stay rows
+    assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 8       # aligned rows <= 512 B -> staged
+    assert lib.tv_tvc_regime(p, 1, 1, 12, 1) == 10         # one 3-vector row -> flat rows
+    assert lib.tv_tvc_regime(p, 1, 1000, 160, 1) == 1      # aligned longer rows stay rows
     assert lib.tv_tvc_regime(p, 1, 1, 2048, 4096) == 3     # columns
     assert lib.tv_tvc_regime(p, 1, 1000, 96, 12) == 4      # small aligned slabs
     assert lib.tv_tvc_regime(p, 1, 1000, 13, 1) == 8       # unaligned short rows -> staged
@@ -184,8 +184,17 @@ def test_library_argument_validation_without_gpu():
     assert lib.tv_tvc_regime(p, 1, 1000, 200, 20) == 4     # width 5 -> slabs
     assert lib.tv_tvc_regime(p + 4, 1, 1000, 96, 12) == 7  # misaligned -> scalar slabs
     assert lib.tv_tvc_regime(p, 0, 1000, 13, 1) == 8       # odd fp64 rows -> staged
-    assert lib.tv_tvc_regime(p, 0, 1000, 131, 1) == 5      # odd fp64 long rows -> scalar rows
+    assert lib.tv_tvc_regime(p, 0, 1000, 131, 1) == 8      # odd fp64 rows <= 2 KB -> staged
+    assert lib.tv_tvc_regime(p, 0, 1000, 301, 1) == 5      # odd fp64 long rows -> scalar rows
     assert lib.tv_tvc_regime(p, 0, 9, 979, 979) == 6       # odd fp64 columns -> scalar columns
+    # the diagnostic override pins a regime only where the view can take it
+    prev = lib.tv_set_regime_override(1)
+    try:
+        assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 1       # rows forced
+        assert lib.tv_tvc_regime(p, 1, 1000, 13, 1) == 8       # rows invalid (unaligned)
+    finally:
+        lib.tv_set_regime_override(prev)
+    assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 8
 
 
 def test_no_oracle_import_in_product():
