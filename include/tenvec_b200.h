@@ -16,6 +16,8 @@
  *   tv_convert      precision.py:109-128 promote / demote (bit-exact semantics)
  *   tv_norm2        kernels.py:234-239  norm2
  *   tv_normalize    kernels.py:242-254  normalize
+ *   tv_tvc_normalize hopm.py:295-333   the last tvc_native of a power-method iteration
+ *                                       + normalize, fused (normalisation in the epilogue)
  *   tv_rank_fold    comm.py:84-100      ring_all_reduce (ascending-rank fold) and
  *                   comm.py:103-134     ring_all_reduce_mixed (chunk c starts at rank c,
  *                                       demote(promote+promote) per hop)
@@ -76,6 +78,20 @@ int tv_tvc(const void* A, int storage, int compute, int64_t u, int64_t nk, int64
  * tv_tvc's regime kernels, used by tvc_looped_oracle (kernels.py:174-188). */
 int tv_tvc_naive(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                  const void* x, double alpha, double beta, void* y, void* stream);
+
+/* The last contraction of a power-method iteration with the vector
+ * normalisation folded into the kernel epilogue (north star; hopm.py:295-333:
+ * tvc_native of the carried 2-mode tensor, then normalize kernels.py:242-254):
+ * y = A x over the contiguous (u, nk, v) view with alpha = 1, beta = 0, then,
+ * in the same launch (the last CTA to finish), y <- demote(promote(y)/||y||)
+ * with tv_normalize's reduction tree; *norm_out (device double) gets the
+ * norm, *status_out (device int32, may be NULL) TV_ENORM on a zero vector
+ * (y then left unscaled).  counter: a device uint32 that is 0 on entry and is
+ * left 0; one per concurrently running call.  For small final products:
+ * u * v <= 2^22 and u * nk * v <= 2^28, else TV_EKERNEL. */
+int tv_tvc_normalize(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
+                     const void* x, void* y, double* norm_out, int32_t* status_out,
+                     unsigned* counter, void* stream);
 
 /* Which kernel regime tv_tvc would pick for this view: 1 rows, 2 short rows,
  * 3 columns, 4 narrow slabs, and their unaligned (scalar-load) forms 5 rows,

@@ -33,6 +33,7 @@ SIGNATURES = {
     "tv_last_error": (ctypes.c_char_p, []),
     "tv_tvc": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),
     "tv_tvc_naive": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),
+    "tv_tvc_normalize": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tv_tvc_regime": (_int, [_vp, _int, _i64, _i64, _i64]),
     "tv_set_regime_override": (_int, [_int]),
     "tv_getvc": (_int, [_int, _vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),

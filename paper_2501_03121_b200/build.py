@@ -19,7 +19,7 @@ CSRC = PKG_DIR / "csrc"
 LIB_DIR = PKG_DIR / "_lib"
 LIB_PATH = LIB_DIR / "libtenvec_b200.so"
 SOURCES = ["tvc.cu", "util.cu"]
-HEADERS = ["tv_types.cuh", "tv_internal.h"]
+HEADERS = ["tv_types.cuh", "tv_internal.h", "tv_norm.cuh"]
 
 NVCC_FLAGS = [
     "-O3",

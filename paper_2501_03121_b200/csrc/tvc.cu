@@ -42,6 +42,7 @@
 #include <type_traits>
 
 #include "tv_internal.h"
+#include "tv_norm.cuh"
 #include "tv_types.cuh"
 
 namespace tv {
@@ -812,6 +813,81 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ------------------------------------------------------- TVC + NORMALIZE ----
+// The last contraction of a dHOPM3 iteration (the carried 2-mode tensor
+// contracted to the iteration's vector, hopm.py:295-319) with the vector
+// normalisation folded into the kernel epilogue (kernels.py:242-254): CTAs of
+// kNormThreads compute the outputs, the LAST CTA to finish (ticket counter,
+// reset on exit) runs the tv_normalize tree over y -- the same bits as
+// tv_normalize on the same y, one launch instead of a TVC, a copy and a norm.
+// Meant for the small final products (<= kTvcNormMax elements): v == 1 ->
+// a warp per row (16-byte loads when aligned); v > 1 -> a CTA per (slab,
+// 32-column block), its 32 warps split n_k and fold in phase order.
+constexpr int64_t kTvcNormMax = 1LL << 22;
+
+template <int SD, typename C, bool AL>
+__global__ void __launch_bounds__(kNormThreads)
+    k_tvc_norm(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+               typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t v, int64_t ncb,
+               double* __restrict__ norm_out, int32_t* __restrict__ status, unsigned* counter) {
+  using T = typename St<SD>::T;
+  constexpr int VEC = VecN<SD>::N;
+  constexpr int NW = kNormThreads / 32;
+  __shared__ C red[NW][33];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (v == 1) {
+    for (int64_t row = (int64_t)blockIdx.x * NW + w; row < u; row += (int64_t)gridDim.x * NW) {
+      const T* rp = A + row * nk;
+      C acc = C(0);
+      if constexpr (AL) {
+        for (int64_t q = lane; q < nk / VEC; q += 32) {
+          C a[VEC];
+          unpack<SD, C>(ld_stream16(rp + q * VEC), a);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc = fma(a[e], promote<SD, C>(x[q * VEC + e]), acc);
+        }
+      } else {
+        for (int64_t j = lane; j < nk; j += 32) acc = fma(promote<SD, C>(rp[j]), promote<SD, C>(x[j]), acc);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) y[row] = epilogue<SD, C>(acc, C(1), C(0), false, y + row);
+    }
+  } else {
+    const int64_t items = u * ncb;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+      const int64_t i = item / ncb;
+      const int64_t l = (item - i * ncb) * 32 + lane;
+      C acc = C(0);
+      if (l < v) {
+        const T* cp = A + i * nk * v + l;
+        for (int64_t j = w; j < nk; j += NW) acc = fma(promote<SD, C>(cp[j * v]), promote<SD, C>(x[j]), acc);
+      }
+      red[w][lane] = acc;
+      __syncthreads();
+      if (w == 0 && l < v) {
+        C s = red[0][lane];
+        const int ph = nk < NW ? (int)nk : NW;
+        for (int q = 1; q < ph; ++q) s += red[q][lane];
+        y[i * v + l] = epilogue<SD, C>(s, C(1), C(0), false, y + i * v + l);
+      }
+      __syncthreads();
+    }
+  }
+  // the last CTA to arrive normalises the whole vector
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  norm_block<SD, C, true>(y, u * v, norm_out, status, 1);
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
 // --------------------------------------------------------------- NAIVE ----
 // the "looped" cross-check (tv_tvc_naive): plain scalar loops, element
 // (i, j, l) at A[i * su + j * sk + l].  v == 1: one warp per row.
@@ -1204,6 +1280,25 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
   return check_launch("tv_tvc");
 }
 
+template <int SD, typename C>
+static int tvc_norm_typed(const void* A, int64_t u, int64_t nk, int64_t v, const void* x, void* y,
+                          double* norm_out, int32_t* status, unsigned* counter, cudaStream_t st) {
+  using T = typename St<SD>::T;
+  constexpr int VEC = VecN<SD>::N;
+  constexpr int NW = kNormThreads / 32;
+  const int64_t ncb = cdiv(v, 32);
+  const int64_t work = v == 1 ? cdiv(u, NW) : u * ncb;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(work, 2LL * sm_count()));
+  const bool al = v == 1 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && nk % VEC == 0;
+  if (al)
+    k_tvc_norm<SD, C, true><<<grid, kNormThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, v, ncb,
+                                                           norm_out, status, counter);
+  else
+    k_tvc_norm<SD, C, false><<<grid, kNormThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, v, ncb,
+                                                            norm_out, status, counter);
+  return check_launch("tv_tvc_normalize");
+}
+
 int tvc_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                  int64_t su, int64_t sk, const void* x, double alpha, double beta, void* y,
                  void* stream, int naive) {
@@ -1243,6 +1338,25 @@ extern "C" int tv_tvc_naive(const void* A, int storage, int compute, int64_t u, 
   if ((u > 0 && (A == nullptr || y == nullptr)) || x == nullptr)
     return tv::set_error(TV_EKERNEL, "tv_tvc_naive: null pointer");
   return tv::tvc_dispatch(A, storage, compute, u, nk, v, nk * v, v, x, alpha, beta, y, stream, 1);
+}
+
+extern "C" int tv_tvc_normalize(const void* A, int storage, int compute, int64_t u, int64_t nk,
+                                int64_t v, const void* x, void* y, double* norm_out,
+                                int32_t* status_out, unsigned* counter, void* stream) {
+  using namespace tv;
+  if (u < 1 || nk < 1 || v < 1) return set_error(TV_EKERNEL, "tv_tvc_normalize: need u, nk, v >= 1");
+  if (!A || !x || !y || !norm_out || !counter) return set_error(TV_EKERNEL, "tv_tvc_normalize: null pointer");
+  if (u * v > kTvcNormMax || u * nk * v > 64 * kTvcNormMax)
+    return set_error(TV_EKERNEL, "tv_tvc_normalize: view too large (use tv_tvc + tv_normalize)");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (mode_id(storage, compute)) {
+    case MODE_F64: return tvc_norm_typed<TV_F64, double>(A, u, nk, v, x, y, norm_out, status_out, counter, st);
+    case MODE_F32: return tvc_norm_typed<TV_F32, float>(A, u, nk, v, x, y, norm_out, status_out, counter, st);
+    case MODE_F32F64: return tvc_norm_typed<TV_F32, double>(A, u, nk, v, x, y, norm_out, status_out, counter, st);
+    case MODE_F16F32: return tvc_norm_typed<TV_F16, float>(A, u, nk, v, x, y, norm_out, status_out, counter, st);
+    case MODE_BF16F32: return tvc_norm_typed<TV_BF16, float>(A, u, nk, v, x, y, norm_out, status_out, counter, st);
+    default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
+  }
 }
 
 extern "C" int tv_tvc_regime(const void* A, int storage, int64_t u, int64_t nk, int64_t v) {

@@ -13,6 +13,7 @@
 #include <string>
 
 #include "tv_internal.h"
+#include "tv_norm.cuh"
 #include "tv_types.cuh"
 
 namespace tv {
@@ -101,40 +102,12 @@ static int convert_from(const void* src, int dst_dt, void* dst, int64_t n, cudaS
 }
 
 // ---------------------------------------------------------------- norm ----
-// one CTA of 1024 threads: strided per-thread sums, xor-shuffle per warp, then
-// warp 0 folds the 32 warp sums -- a fixed tree, so every rank that holds the
-// same vector computes the same bits (hopm.py:339-342 checks exactly that).
+// one CTA of kNormThreads: the fixed tree of tv_norm.cuh
 template <int SD, typename C>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(kNormThreads)
     k_norm(typename St<SD>::T* __restrict__ x, int64_t n, double* __restrict__ norm_out,
            int32_t* __restrict__ status, int do_scale) {
-  __shared__ C part[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  C s = C(0);
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const C c = promote<SD, C>(x[i]);
-    s = fma(c, c, s);
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) part[w] = s;
-  __syncthreads();
-  if (w == 0) {
-    s = lane < (int)(blockDim.x >> 5) ? part[lane] : C(0);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) part[0] = s;
-  }
-  __syncthreads();
-  const C nrm = sqrt(part[0]);
-  if (threadIdx.x == 0) {
-    norm_out[0] = (double)nrm;
-    if (status) status[0] = (nrm == C(0)) ? TV_ENORM : TV_OK;
-  }
-  if (do_scale && nrm != C(0)) {
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-      x[i] = demote<SD, C>(promote<SD, C>(x[i]) / nrm);
-  }
+  norm_block<SD, C, false>(x, n, norm_out, status, do_scale);
 }
 
 static int norm_dispatch(void* x, int storage, int compute, int64_t n, double* norm_out,
@@ -143,11 +116,11 @@ static int norm_dispatch(void* x, int storage, int compute, int64_t n, double* n
   if (n < 0 || norm_out == nullptr || (n > 0 && x == nullptr))
     return set_error(TV_EKERNEL, "tv_norm: bad arguments");
   switch (mode_id(storage, compute)) {
-    case MODE_F64: k_norm<TV_F64, double><<<1, 1024, 0, st>>>((double*)x, n, norm_out, status, do_scale); break;
-    case MODE_F32: k_norm<TV_F32, float><<<1, 1024, 0, st>>>((float*)x, n, norm_out, status, do_scale); break;
-    case MODE_F32F64: k_norm<TV_F32, double><<<1, 1024, 0, st>>>((float*)x, n, norm_out, status, do_scale); break;
-    case MODE_F16F32: k_norm<TV_F16, float><<<1, 1024, 0, st>>>((uint16_t*)x, n, norm_out, status, do_scale); break;
-    case MODE_BF16F32: k_norm<TV_BF16, float><<<1, 1024, 0, st>>>((uint16_t*)x, n, norm_out, status, do_scale); break;
+    case MODE_F64: k_norm<TV_F64, double><<<1, kNormThreads, 0, st>>>((double*)x, n, norm_out, status, do_scale); break;
+    case MODE_F32: k_norm<TV_F32, float><<<1, kNormThreads, 0, st>>>((float*)x, n, norm_out, status, do_scale); break;
+    case MODE_F32F64: k_norm<TV_F32, double><<<1, kNormThreads, 0, st>>>((float*)x, n, norm_out, status, do_scale); break;
+    case MODE_F16F32: k_norm<TV_F16, float><<<1, kNormThreads, 0, st>>>((uint16_t*)x, n, norm_out, status, do_scale); break;
+    case MODE_BF16F32: k_norm<TV_BF16, float><<<1, kNormThreads, 0, st>>>((uint16_t*)x, n, norm_out, status, do_scale); break;
     default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
   }
   return check_launch("tv_norm");

@@ -174,6 +174,46 @@ def tvc_native(
     return Tensor(out_shape, ybuf, mode)
 
 
+TVC_NORM_MAX = 1 << 22  # kTvcNormMax in tvc.cu: outputs of a fused TVC + normalize
+
+
+def tvc_normalize_fits(t: Tensor, k: int) -> bool:
+    """Whether tv_tvc_normalize takes this contraction (a small final product)."""
+    md = matricize_dims(t.shape, k)
+    return md.u * md.v <= TVC_NORM_MAX and t.size <= 64 * TVC_NORM_MAX
+
+
+def tvc_normalize_async(t: Tensor, x, k: int, out: torch.Tensor, norm_slot: torch.Tensor,
+                        status_slot: torch.Tensor | None, counter: torch.Tensor,
+                        counters: KernelCounters | None = None) -> Tensor:
+    """The last contraction of a power-method iteration with the normalisation
+    folded into the kernel epilogue (tv_tvc_normalize): out <- t x_k scaled to
+    unit norm, the norm it had into ``norm_slot`` (device float64), TV_ENORM
+    into ``status_slot`` on a zero vector; no host sync.  Same bits as
+    ``tvc_native`` into out followed by ``normalize(out)`` up to the TVC's
+    summation order.  ``counter`` is a zeroed device int32 the kernel leaves
+    zeroed.  Counted like the two calls it replaces (kernels.py:168-170,
+    234-254)."""
+    md = matricize_dims(t.shape, k)
+    if tuple(x.shape) != (md.nk,):
+        raise KernelError(f"vector of {tuple(x.shape)} for mode {k} of extent {md.nk}")
+    out_shape = t.shape.drop(k)
+    n = out_shape.size
+    mode = t.mode
+    if out.numel() < n or out.dtype != mode.torch_storage or not out.is_cuda:
+        raise KernelError("out must be a CUDA tensor in the storage format with room for the vector")
+    ybuf = out[:n]
+    xv = _vec(x, mode, "x")
+    sp = status_slot.data_ptr() if status_slot is not None else None
+    lib = _lib.load()
+    _lib.check(lib.tv_tvc_normalize(t.buf.data_ptr(), mode.tv_storage, mode.tv_compute, md.u, md.nk,
+                                    md.v, xv.data_ptr(), ybuf.data_ptr(), norm_slot.data_ptr(), sp,
+                                    counter.data_ptr(), _lib.stream_ptr()), "tvc_normalize")
+    if counters is not None:
+        counters.count("tvc", t.size + md.nk, n, mode.storage_bytes)
+    return Tensor(out_shape, ybuf, mode)
+
+
 def tvc_regime(t: Tensor, k: int) -> str:
     """Name of the kernel regime tv_tvc picks for mode k of t."""
     md = matricize_dims(t.shape, k)

@@ -4,7 +4,7 @@ KEYS='Kernel Name|gpu__time_duration.sum|dram__bytes_read.sum|dram__bytes_write.
 run() {  # name shape mode k
   name=$1; shape=$2; mode=$3; k=$4
   python scripts/tvc_one.py --shape $shape --mode $mode --k $k > gpurun_out/ncu_suite/one_$name.log 2>&1 && \
-  ncu --set full --clock-control none -k regex:"k_(rows|cols|slabs|staged)" -s 1 -c 1 -o /tmp/p_$name python scripts/tvc_one.py --shape $shape --mode $mode --k $k > gpurun_out/ncu_suite/ncu_$name.log 2>&1
+  ncu --set full --clock-control none -k regex:"k_(rows|cols|slabs|staged|flat)" -s 1 -c 1 -o /tmp/p_$name python scripts/tvc_one.py --shape $shape --mode $mode --k $k > gpurun_out/ncu_suite/ncu_$name.log 2>&1
   echo $name rc=$?
   ncu -i /tmp/p_$name.ncu-rep --page raw --csv > /tmp/raw_$name.csv 2>/dev/null
   python - "$name" "$KEYS" <<'PY'
@@ -31,6 +31,9 @@ run rows_f32_c3p8_k4 96,96,96,96,12 f32 4
 run slabs_u_f32_k1 20000,300,21 f32 1
 run staged_f64_13p8_k6 13,13,13,13,13,13,13,13 f64 6
 run staged_f64_13p8_k7 13,13,13,13,13,13,13,13 f64 7
+run staged_f64_175p4_k3 175,175,175,175 f64 3
+run staged_f64_63p5_k3 63,63,63,63,63 f64 3
+run flat_f32_c3_k3 96,96,96,96,96 f32 3
 run cols_bf16_c5p8_k1 4096,4096,512 bf16f32 1
 run rows_bf16_c5p8_k2 4096,4096,512 bf16f32 2
 run cols_f32f64_k0 512,512,512 f32f64 0

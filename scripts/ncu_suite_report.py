@@ -58,7 +58,7 @@ def main(out_dir: str = "gpurun_out/ncu_suite") -> None:
                      f"{alg / t / 1e9 / peak * 100:.0f}%" if alg else "-",
                      f"{dram / 1e9:.2f}", f"{dram / alg:.3f}" if alg else "-",
                      f"{num(r[idx['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']]):.1f}",
-                     f"{eff:.2f}" if eff == eff else "-",
+                     "TMA" if "k_staged" in kern else (f"{eff:.2f}" if eff == eff else "-"),
                      f"{num(r[idx['sm__warps_active.avg.pct_of_peak_sustained_active']]):.0f}",
                      f"{num(r[idx['smsp__issue_active.avg.pct_of_peak_sustained_active']]):.0f}",
                      r[idx["launch__registers_per_thread"]]]
