@@ -52,7 +52,7 @@ WORKLOADS = {
     "c2": dict(desc="C2: 2048^3 fp64 TVC mode sweep k=0,1,2 (dTVC, split s=0 over N GPUs)",
                shape=(2048, 2048, 2048), mode="f64", s=0, kind="sweep"),
     "c1": dict(desc="C1: 256^3 fp64 TVC mode sweep k=0,1,2 (L2-flushed between steps)",
-               shape=(256, 256, 256), mode="f64", s=0, kind="sweep", flush=True),
+               shape=(256, 256, 256), mode="f64", s=0, kind="sweep", flush=True, graph=True),
     "c3": dict(desc="C3: 96^5 fp32 dTVC mode sweep k=0..4, split s=4 over N GPUs",
                shape=(96,) * 5, mode="f32", s=4, kind="sweep"),
     "c4": dict(desc="C4: dHOPM3 384^4 fp64, split s=3 over N GPUs, one step = one sweep",
@@ -262,14 +262,20 @@ def run_ours(args) -> dict | None:
             comm_bytes += 2 * out_r * sb * (world - 1) // world  # sent per rank (a2a + gather)
     flush = None
     if wl.get("flush"):
-        flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        flush = L2Flush(torch.device("cuda"))
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
 
+    use_graph = world == 1 and bool(args.graph if args.graph is not None else wl.get("graph"))
+    sweep_graph = tv.SweepGraph(dt, xs) if use_graph else None
+
     def step():
         # one mode sweep through the public API; at N > 1 the split-mode
-        # reduction runs on a side stream under the other modes' streaming
+        # reduction runs on a side stream under the other modes' streaming;
+        # launch-bound sizes replay the sweep as one captured CUDA graph
+        if sweep_graph is not None:
+            return sweep_graph.replay()
         return tv.dtvc_sweep(dt, xs)
 
     for _ in range(args.warmup):
@@ -283,7 +289,7 @@ def run_ours(args) -> dict | None:
     torch.cuda.synchronize()
     for i in range(args.steps):
         if flush is not None:
-            flush.zero_()
+            flush()
         ev[i][0].record()
         step()
         ev[i][1].record()
@@ -307,7 +313,11 @@ def run_ours(args) -> dict | None:
     for _ in range(max(3, min(args.steps, 10))):
         for k in range(d):
             if flush is not None:
-                flush.zero_()
+                flush()
+            # a blocking kernel ahead of the start event (nvbench's recipe) keeps
+            # the stream busy while the host enqueues the launch, so the event
+            # pair brackets GPU execution, not Python launch latency
+            _block_stream(torch)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             tv.dtvc(dt, xs[k], k, defer=(k == s and world > 1))
@@ -347,9 +357,11 @@ def run_ours(args) -> dict | None:
         "dtype": "f64" if mode.name == "f64" else mode.name,
         "data": "synthetic (hash fill in [1,97] generated on device from the global index)",
         "config": {"workload": wl["desc"], "shape": list(shape.extents), "precision": mode.name,
-                   "split_mode": s, "p": world, "l2": "flushed between steps" if flush is not None
+                   "split_mode": s, "p": world, "l2": L2Flush.DESC if flush is not None
                    else "tensor (%.1f GB/GPU) >> 126 MB L2, no flush" % (part.size * sb / 1e9),
-                   "parallelism": f"split{world}"},
+                   "parallelism": f"split{world}",
+                   "launch": "CUDA graph replay of the sweep (tv.SweepGraph)" if use_graph
+                   else "eager public API (tv.dtvc_sweep)"},
         "per_gpu_gbs": round(value / world, 2),
         "roofline_frac_aggregate": round(value / (peak * world), 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -371,6 +383,38 @@ def run_ours(args) -> dict | None:
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = {k: v for k, v in cpu_reference(args.workload).items() if k != "ms_per_step"}
     return line
+
+
+def _block_stream(torch, cycles: int = 2_000_000) -> None:
+    """~1 ms of device-side spinning on the current stream (torch.cuda._sleep)."""
+    if hasattr(torch.cuda, "_sleep"):
+        torch.cuda._sleep(cycles)
+
+
+class L2Flush:
+    """Evict the tensor from the 126 MB L2 between timed steps, untimed: write
+    512 MB (the classic flush), then stream-read another 512 MB so the flush's
+    own dirty lines are written back here rather than inside the next timed
+    kernel (which would charge it ~126 MB of foreign DRAM writes)."""
+
+    DESC = ("flushed between steps: 512 MB write + 512 MB read pass, both untimed "
+            "(L2 holds neither the tensor nor dirty flush lines when a step starts)")
+
+    def __init__(self, device):
+        import torch
+
+        from paper_2501_03121_b200 import _lib
+
+        self._lib = _lib
+        self.w = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+        self.r = torch.zeros(512 << 20, dtype=torch.uint8, device=device)
+        self.sink = torch.zeros(4, dtype=torch.int32, device=device)
+
+    def __call__(self) -> None:
+        self.w.zero_()
+        lib = self._lib.load()
+        self._lib.check(lib.tv_read_stream(self.r.data_ptr(), self.r.numel(), self.sink.data_ptr(),
+                                           self._lib.stream_ptr()))
 
 
 def read_stream_gbs(buf) -> float:
@@ -528,6 +572,9 @@ def main(argv=None) -> int:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", type=int, default=None,
+                    help="1: time the sweep as a captured CUDA graph (tv.SweepGraph; one GPU only); "
+                         "default: on for launch-bound workloads (c1)")
     ap.add_argument("--shape", default=None, help="override the workload shape, e.g. 1024,1024,1024 (profiling)")
     args = ap.parse_args(argv)
     if args.shape:
