@@ -343,3 +343,23 @@ def test_initial_vectors(tv):
     b = O.initial_vectors((5, 5), "f64", kind="random", seed=7)
     for u, v in zip(a, b):
         assert np.allclose(u, v, rtol=1e-15, atol=1e-16)
+
+
+def test_sweep_graph_replays_the_eager_sweep(tv):
+    """tv.SweepGraph: the captured sweep equals dtvc_sweep bitwise, and a replay
+    with new vectors equals the eager sweep on those vectors."""
+    for name, shape in (("f64", (33, 40, 17)), ("bf16f32", (16, 24, 8, 5))):
+        mode = tv.MODES[name]
+        dt = tv.distribute_generated(tv.Shape(shape), 0, 1, mode, fill="hash", seed=3)
+        rng = np.random.default_rng(4)
+        xs = [O.demote(rng.standard_normal(n), name).copy() for n in shape]
+        g = tv.SweepGraph(dt, xs)
+        got = g.replay()
+        want = tv.dtvc_sweep(dt, xs)
+        for k in range(len(shape)):
+            assert np.array_equal(_bits(got[k].parts[0].to_numpy()), _bits(want[k].parts[0].to_numpy()))
+        xs2 = [O.demote(rng.standard_normal(n), name).copy() for n in shape]
+        got = g.replay(xs2)
+        want = tv.dtvc_sweep(dt, xs2)
+        for k in range(len(shape)):
+            assert np.array_equal(_bits(got[k].parts[0].to_numpy()), _bits(want[k].parts[0].to_numpy()))
