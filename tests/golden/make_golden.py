@@ -32,9 +32,14 @@ MODE_SHAPES = [(7,), (3, 5), (5, 8), (4, 6, 5), (2, 3, 4, 5), (6, 1, 9), (3, 40,
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
+    ap.add_argument("--only", default="all", choices=["all", "costmodel"])
     args = ap.parse_args()
     sys.path.insert(0, args.ref)
     import tenvec as T  # the reference package
+
+    costmodel()
+    if args.only == "costmodel":
+        return
 
     # -- precision ---------------------------------------------------------
     spots = np.array([1.0, np.pi, 2.0, -1.5, 1e-38, 1.1754944e-38, 65504.0, 3.0e38, -7.25e-5,
@@ -229,6 +234,54 @@ def main() -> None:
     out["n"] = np.array(c)
     np.savez_compressed(HERE / "hopm.npz", **out)
     print("golden fixtures written to", HERE)
+
+
+def costmodel() -> None:
+    """The reference's closed-form streamed-memory model (costmodel.py:56-320)
+    over a grid of (d, n, p, s): every rational as (numerator, denominator)."""
+    import tenvec.costmodel as C
+
+    meta, ints, fracs, mpar = [], [], [], []
+    for d in range(2, 7):
+        for n in (1, 2, 3, 5, 8):
+            for p in (1, 2, 3, 4, 8):
+                for s in range(d):
+                    r = C.cost_report(d, n, p, s)
+                    meta.append((d, n, p, s))
+                    ints.append(r.m_seq)
+                    shift = C.splitting_shift_residual(d, n, p, s) if s >= 1 else 0
+                    row = [r.M_par, r.M_par_min, r.eta_inv, r.H_inv, r.ring_overhead,
+                           C.M_par_bracketed(d, n, p, s)]
+                    row += [C.Fraction(shift)]
+                    fracs.append([(f.numerator, f.denominator) for f in row])
+                    for j in range(d):
+                        for div in ("ceiling", "exact"):
+                            br, ap_ = C.m_par(d, n, p, s, j, div)
+                            mpar.append((d, n, p, s, j, div == "exact", br.numerator, br.denominator,
+                                         ap_.numerator, ap_.denominator))
+    np.savez_compressed(HERE / "costmodel.npz", meta=np.array(meta), m_seq=np.array(ints),
+                        fracs=np.array(fracs, dtype=np.int64), m_par=np.array(mpar, dtype=np.int64))
+    # the `cost` subcommand's CSV (cli.py:147-156, bench.py:336-409)
+    import contextlib
+    import io
+    import json
+    from tenvec.cli import main as ref_cli
+    records = []
+    for argv in (["cost", "--dims", "8^5", "--split", "0", "--workers", "4"],
+                 ["cost", "--dims", "384^4", "--split", "3", "--workers", "8"],
+                 ["cost", "--dims", "979^3", "--split", "2", "--workers", "8"],
+                 ["cost", "--dims", "paper:d4", "--split", "1", "--workers", "3"],
+                 ["cost", "--dims", "desk:d5", "--split", "4", "--workers", "5", "--csv", "-"],
+                 ["cost", "--dims", "7^2"],
+                 ["cost", "--dims", "2,3,4", "--workers", "2"],
+                 ["cost", "--dims", "8^3", "--split", "3", "--workers", "2"],
+                 ["cost", "--dims", "8^3", "--workers", "0"]):
+        argv = [a for a in argv if a not in ("--csv", "-")]
+        buf, err = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(buf), contextlib.redirect_stderr(err):
+            rc = ref_cli(argv)
+        records.append({"argv": argv, "rc": rc, "stdout": buf.getvalue()})
+    (HERE / "cli_cost.json").write_text(json.dumps(records, indent=1) + "\n")
 
 
 if __name__ == "__main__":

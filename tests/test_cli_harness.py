@@ -29,9 +29,15 @@ def test_configuration_errors_exit_2_without_a_gpu(case):
     assert rc == case["rc"] == 2 and out == case["stdout"] and "configuration error" in err
 
 
-def test_cost_subcommand_is_a_configuration_error():
-    rc, _, err = _run(["cost"])
-    assert rc == 2 and "not part of" in err
+COST_CASES = json.loads((GOLDEN / "cli_cost.json").read_text())
+
+
+@pytest.mark.parametrize("case", COST_CASES, ids=lambda c: " ".join(c["argv"][1:]))
+def test_cost_subcommand_byte_identical_to_reference(case):
+    """`cost` evaluates the closed forms (no GPU): same CSV bytes and exit
+    codes as the reference CLI (cli.py:147-156)."""
+    rc, out, err = _run(case["argv"])
+    assert rc == case["rc"] and out == case["stdout"], err
 
 
 @pytest.mark.gpu

@@ -363,3 +363,25 @@ def test_sweep_graph_replays_the_eager_sweep(tv):
         want = tv.dtvc_sweep(dt, xs2)
         for k in range(len(shape)):
             assert np.array_equal(_bits(got[k].parts[0].to_numpy()), _bits(want[k].parts[0].to_numpy()))
+
+
+def test_classical_counters_equal_closed_forms(tv):
+    """The classical schedule's device counters against Eqs. (3)-(6)
+    (costmodel.py:56-115; test_acceptance.py:111-128): canonical sweeps stream
+    m_seq per iteration, classical distributed sweeps the bracketed m_par per
+    rank and iteration."""
+    from paper_2501_03121_b200 import schedule as S
+
+    rng = np.random.default_rng(9)
+    for d in range(2, 6):
+        A = tv.Tensor.from_array(rng.integers(1, 5, (8,) * d).astype(float))
+        res = tv.hopm_canonical(A, sweeps=1)
+        assert res.iteration_touched[0] == [S.m_seq(d, 8)] * d, d
+    for d in (3, 4):
+        A = tv.Tensor.from_array(rng.integers(1, 5, (8,) * d).astype(float))
+        for p in (1, 2, 4):
+            for s in range(d):
+                res = tv.dhopm3(tv.distribute(A, s, p), sweeps=1, reuse=False)
+                for r in range(p):
+                    for j in range(d):
+                        assert res.iteration_touched[r][j] == S.m_par(d, 8, p, s, j)[0], (d, p, s, r, j)
