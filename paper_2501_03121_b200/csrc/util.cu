@@ -132,33 +132,65 @@ struct Srcs {
 };
 
 template <int SD, typename C>
-__global__ void k_fold(Srcs srcs, int p, int64_t n, int64_t chunk, int start, int mixed,
-                       typename St<SD>::T* __restrict__ dst) {
+__device__ __forceinline__ typename St<SD>::T fold_hop(typename St<SD>::T cur, typename St<SD>::T b,
+                                                       int mixed) {
+  if constexpr (SD == TV_F64 || SD == TV_F32) {
+    if (!mixed) return add_rn(cur, b);  // ascending-rank fold in the storage format (comm.py:95-97)
+  }
+  // narrow storage, or the mixed ring: demote(promote + promote) per hop (comm.py:123-130)
+  return demote<SD, C>(add_rn(promote<SD, C>(cur), promote<SD, C>(b)));
+}
+
+// Element e folds the p sources in rank order r0, r0+1, ... (mod p): r0 = 0
+// for the exact fold, (start + e / chunk) % p for the mixed ring.  16-byte
+// vectors of VEC elements when every pointer is aligned; a vector whose
+// elements straddle a ring chunk boundary (different r0) folds per element.
+template <int SD, typename C>
+__global__ void __launch_bounds__(256)
+    k_fold(Srcs srcs, int p, int64_t n, int64_t chunk, int start, int mixed,
+           typename St<SD>::T* __restrict__ dst, int vec_ok) {
   using T = typename St<SD>::T;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    T cur;
-    if (!mixed) {
-      // ascending-rank fold in the storage format (comm.py:95-97)
-      cur = reinterpret_cast<const T*>(srcs.p[0])[e];
-      for (int r = 1; r < p; ++r) {
-        const T b = reinterpret_cast<const T*>(srcs.p[r])[e];
-        if constexpr (SD == TV_F64 || SD == TV_F32) cur = add_rn(cur, b);
-        else cur = demote<SD, C>(add_rn(promote<SD, C>(cur), promote<SD, C>(b)));
-      }
-    } else {
-      // chunk c starts at rank c, each hop demote(promote + promote) (comm.py:123-130)
-      const int64_t c = chunk > 0 ? e / chunk : 0;
-      const int r0 = (int)((start + c) % p);
-      cur = reinterpret_cast<const T*>(srcs.p[r0])[e];
-      for (int i = 1; i < p; ++i) {
-        const int r = (r0 + i) % p;
-        const T b = reinterpret_cast<const T*>(srcs.p[r])[e];
-        cur = demote<SD, C>(add_rn(promote<SD, C>(cur), promote<SD, C>(b)));
-      }
+  constexpr int VEC = VecN<SD>::N;
+  auto r0_of = [&](int64_t e) -> int {
+    if (!mixed) return 0;
+    const int64_t c = chunk > 0 ? e / chunk : 0;
+    return (int)((start + c) % p);
+  };
+  auto one = [&](int64_t e) {
+    const int r0 = r0_of(e);
+    T cur = reinterpret_cast<const T*>(srcs.p[r0])[e];
+    for (int i = 1; i < p; ++i) {
+      const int r = r0 + i < p ? r0 + i : r0 + i - p;
+      cur = fold_hop<SD, C>(cur, reinterpret_cast<const T*>(srcs.p[r])[e], mixed);
     }
     dst[e] = cur;
+  };
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t done = 0;
+  if (vec_ok) {
+    const int64_t nv = n / VEC;
+    for (int64_t q = i0; q < nv; q += stride) {
+      const int64_t e0 = q * VEC;
+      const int r0 = r0_of(e0);
+      if (mixed && r0_of(e0 + VEC - 1) != r0) {  // straddles a ring chunk boundary
+#pragma unroll 1
+        for (int k = 0; k < VEC; ++k) one(e0 + k);
+        continue;
+      }
+      Pack16<SD> cur, b;
+      cur.u = ld_stream16(reinterpret_cast<const uint4*>(srcs.p[r0]) + q);
+      for (int i = 1; i < p; ++i) {
+        const int r = r0 + i < p ? r0 + i : r0 + i - p;
+        b.u = ld_stream16(reinterpret_cast<const uint4*>(srcs.p[r]) + q);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) cur.e[k] = fold_hop<SD, C>(cur.e[k], b.e[k], mixed);
+      }
+      reinterpret_cast<uint4*>(dst)[q] = cur.u;
+    }
+    done = nv * VEC;
   }
+  for (int64_t e = done + i0; e < n; e += stride) one(e);
 }
 
 static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int start, int storage,
@@ -167,13 +199,16 @@ static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int sta
   if (p < 1 || p > TV_MAX_RANKS || n < 0 || start < 0 || chunk < 0)
     return set_error(TV_ECOLL, "tv_rank_fold: bad rank count / length / chunk");
   if (n == 0) return TV_OK;
-  const unsigned g = grid_1d(n, 256);
+  int v = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  for (int r = 0; r < p; ++r) v &= (reinterpret_cast<uintptr_t>(s.p[r]) & 15) == 0;
+  const int sb = dtype_bytes(storage);
+  const unsigned g = grid_1d(v && sb > 0 ? (n * sb + 15) / 16 : n, 256);
   switch (mode_id(storage, compute)) {
-    case MODE_F64: k_fold<TV_F64, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (double*)dst); break;
-    case MODE_F32: k_fold<TV_F32, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (float*)dst); break;
-    case MODE_F32F64: k_fold<TV_F32, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (float*)dst); break;
-    case MODE_F16F32: k_fold<TV_F16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (uint16_t*)dst); break;
-    case MODE_BF16F32: k_fold<TV_BF16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (uint16_t*)dst); break;
+    case MODE_F64: k_fold<TV_F64, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (double*)dst, v); break;
+    case MODE_F32: k_fold<TV_F32, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (float*)dst, v); break;
+    case MODE_F32F64: k_fold<TV_F32, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (float*)dst, v); break;
+    case MODE_F16F32: k_fold<TV_F16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (uint16_t*)dst, v); break;
+    case MODE_BF16F32: k_fold<TV_BF16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (uint16_t*)dst, v); break;
     default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
   }
   return check_launch("tv_rank_fold");
