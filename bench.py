@@ -361,7 +361,10 @@ def run_ours(args) -> dict | None:
                    else "tensor (%.1f GB/GPU) >> 126 MB L2, no flush" % (part.size * sb / 1e9),
                    "parallelism": f"split{world}",
                    "launch": "CUDA graph replay of the sweep (tv.SweepGraph)" if use_graph
-                   else "eager public API (tv.dtvc_sweep)"},
+                   else "eager public API (tv.dtvc_sweep)",
+                   "split_reduction": None if group is None else (
+                       "fused: TVC writes owner ranges into peer memory, owner fold, peer gather"
+                       if group.algo == "fused" else group.algo)},
         "per_gpu_gbs": round(value / world, 2),
         "roofline_frac_aggregate": round(value / (peak * world), 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -146,6 +146,15 @@ int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64
                          int64_t chunk, int start, int storage, int compute, int mixed,
                          void* dst, void* stream);
 
+/* tv_rank_fold_strided over a RANGE [offset, offset + n) of a ring buffer
+ * whose ring chunks have ring_chunk elements (chunk c starts at rank c, the
+ * mixed ring of comm.py:103-134; ignored for the exact fold): the owner of a
+ * range folds the p partial copies of it that peers wrote into its receive
+ * slots (src + r * src_stride_elems), in the reference's per-element order. */
+int tv_rank_fold_range(const void* src, int64_t src_stride_elems, int p, int64_t n,
+                       int64_t ring_chunk, int64_t offset, int storage, int compute, int mixed,
+                       void* dst, void* stream);
+
 /* dst[e] = srcs[e / chunk][e] (srcs a HOST array of p device pointers, e.g.
  * peer buffers of a symmetric-memory group): the gather phase of the
  * peer-memory allreduce, where rank r's buffer holds reduced ring chunk r. */

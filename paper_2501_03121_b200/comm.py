@@ -29,6 +29,7 @@ from __future__ import annotations
 import ctypes
 import threading
 import time
+import warnings
 from dataclasses import dataclass
 from typing import Callable
 
@@ -326,7 +327,7 @@ class RankGroup:
     multi-process tests inject a host fold to exercise the chunk logic over
     gloo without a GPU.
 
-    ``algo`` (default from TENVEC_B200_ALLREDUCE, else "exact"):
+    ``algo`` (default from TENVEC_B200_ALLREDUCE, else "fused"):
       exact  all-to-all of ring chunks + fold kernel + all-gather (NCCL moves
              the bytes), reference-exact;
       p2p    the same fold over PEER memory: every rank's buffer is a
@@ -334,7 +335,14 @@ class RankGroup:
              folds ring chunk c straight from its peers' buffers with the fold
              kernel, a select kernel gathers the reduced chunks; three device
              barriers, no NCCL, reference-exact;
-      nccl   ncclAllReduce (rank-consistent, not reference-ordered).
+      nccl   ncclAllReduce (rank-consistent, not reference-ordered);
+      fused  for dtvc's split-mode contraction (k == s): the TVC itself writes
+             each owner's output range straight into that owner's receive slot
+             in peer (symmetric) memory over NVLink, the owner folds its p
+             slots in the reference order, and every rank gathers the reduced
+             ranges from its peers (``tvc_reduce_fused``); no NCCL, no partial
+             written to local HBM first.  Other reductions run as "exact";
+             without symmetric memory the group falls back to "exact".
     """
 
     def __init__(self, group=None, *, algo: str | None = None, fold: FoldFn | None = None):
@@ -344,8 +352,8 @@ class RankGroup:
 
         if not dist.is_initialized():
             raise CollectiveError("torch.distributed is not initialised")
-        algo = algo or os.environ.get("TENVEC_B200_ALLREDUCE", "exact")
-        if algo not in ("exact", "nccl", "p2p"):
+        algo = algo or os.environ.get("TENVEC_B200_ALLREDUCE", "fused")
+        if algo not in ("exact", "nccl", "p2p", "fused"):
             raise CollectiveError(f"unknown allreduce algorithm {algo!r}")
         self._dist = dist
         self.group = group
@@ -393,6 +401,87 @@ class RankGroup:
         srcs = (ctypes.c_void_p * p)(*ptrs)
         _lib.check(lib.tv_rank_select(srcs, p, n, q, st, buf.data_ptr(), stream), "p2p gather")
         hdl.barrier(channel=0)                      # peers done reading this buffer
+
+    def tvc_reduce_fused(self, part, xv: torch.Tensor, k: int, mode: PrecisionMode,
+                         counters: list[CommCounters] | None = None,
+                         finish_stream: torch.cuda.Stream | None = None) -> torch.Tensor | None:
+        """dtvc's split-mode contraction fused with its reduction over peer
+        memory (algo="fused").  The (u, n_k, v) output is cut into p owner
+        ranges -- slab ranges when u >= p, column ranges when u == 1 -- and
+        this rank's TVC launches write range c directly into rank c's receive
+        slot for this rank (a peer pointer: the stores cross NVLink).  After a
+        device barrier the owner folds its p slots (ascending rank / the mixed
+        ring's per-element order, comm.py:84-134, the same bits as every other
+        algorithm), and after a second barrier every rank gathers the p reduced
+        ranges from the owners.  Returns the replicated output, or None when
+        the view has no owner partition (1 < u < p) and the caller falls back.
+        With ``finish_stream`` the fold and gather run there (the caller waits
+        on it before reading the output), overlapping later work."""
+        from .tensor import matricize_dims
+
+        p, rank = self.size, self.rank
+        md = matricize_dims(part.shape, k)
+        u, nk, v = md.u, md.nk, md.v
+        n = u * v
+        if p == 1 or not (u >= p or u == 1):
+            return None
+        sb = mode.storage_bytes
+        along_u = u >= p
+        outer = u if along_u else v
+        q = -(-outer // p)  # owner c holds outer indices [c q, (c+1) q)
+        unit = v if along_u else 1  # output elements per outer index
+        chunk = q * unit  # output elements per owner (the last one may be short)
+        bounds = [(min(c * q, outer), min((c + 1) * q, outer)) for c in range(p)]
+        sizes = [(b - a) * unit for a, b in bounds]
+        ring = ring_chunks(n, p)
+        slot_bytes = -(-chunk * sb // 16) * 16
+        try:
+            sym, hdl = self._symmetric((p + 1) * slot_bytes, part.buf.device)
+        except Exception as exc:  # noqa: BLE001 - no symmetric memory here: NCCL transport
+            warnings.warn(f"RankGroup: peer memory unavailable ({exc!r:.200}); using algo='exact'")
+            self.algo = "exact"
+            return None
+        counters = self.counters if counters is None else counters
+        for cc in counters:
+            cc.collective_calls += 1
+        _charge_allreduce_movement(counters, [b - a for a, b in ring], p)
+        ptrs = [int(ptr) for ptr in hdl.buffer_ptrs]
+        lib = _lib.load()
+        stream = _lib.stream_ptr()
+        st_, ct_ = mode.tv_storage, mode.tv_compute
+        a_ptr = part.buf.data_ptr()
+        hdl.barrier(channel=0)  # peers are done with the previous call's slots
+        for j in range(p):  # own range first, then the peers in ring order
+            c = (rank + j) % p
+            lo, hi = bounds[c]
+            if hi <= lo:
+                continue
+            dst = ptrs[c] + rank * slot_bytes
+            if along_u:
+                rc = lib.tv_tvc(a_ptr + lo * nk * v * sb, st_, ct_, hi - lo, nk, v, xv.data_ptr(),
+                                1.0, 0.0, dst, stream)
+            else:  # u == 1: columns [lo, hi) of the nk x v slab, a strided vecmat
+                rc = lib.tv_getvc(1, a_ptr + lo * sb, st_, ct_, nk, hi - lo, v, xv.data_ptr(),
+                                  1.0, 0.0, dst, stream)
+            _lib.check(rc, "fused dtvc: contraction into peer memory")
+        out = torch.empty(n, dtype=mode.torch_storage, device=part.buf.device)
+        if finish_stream is not None:
+            finish_stream.wait_stream(torch.cuda.current_stream())
+            out.record_stream(finish_stream)
+        with torch.cuda.stream(finish_stream or torch.cuda.current_stream()):
+            stream = _lib.stream_ptr()
+            hdl.barrier(channel=0)  # every slot holds its writer's partial range
+            mine = sizes[rank]
+            if mine:
+                _lib.check(lib.tv_rank_fold_range(sym.data_ptr(), slot_bytes // sb, p, mine,
+                                                  ring[0][1] - ring[0][0], rank * chunk, st_, ct_,
+                                                  int(mode.mixed), sym.data_ptr() + p * slot_bytes,
+                                                  stream), "fused dtvc: owner fold")
+            hdl.barrier(channel=0)  # every owner's reduced range is ready
+            srcs = (ctypes.c_void_p * p)(*[ptrs[c] + p * slot_bytes - c * chunk * sb for c in range(p)])
+            _lib.check(lib.tv_rank_select(srcs, p, n, chunk, st_, out.data_ptr(), stream),
+                       "fused dtvc: gather")
+        return out
 
     def _check_rank(self, rank: int) -> None:
         if rank != self.rank:

@@ -142,18 +142,19 @@ __device__ __forceinline__ typename St<SD>::T fold_hop(typename St<SD>::T cur, t
 }
 
 // Element e folds the p sources in rank order r0, r0+1, ... (mod p): r0 = 0
-// for the exact fold, (start + e / chunk) % p for the mixed ring.  16-byte
+// for the exact fold, (start + (off + e) / chunk) % p for the mixed ring (off:
+// where this range sits in the ring buffer).  16-byte
 // vectors of VEC elements when every pointer is aligned; a vector whose
 // elements straddle a ring chunk boundary (different r0) folds per element.
 template <int SD, typename C>
 __global__ void __launch_bounds__(256)
-    k_fold(Srcs srcs, int p, int64_t n, int64_t chunk, int start, int mixed,
+    k_fold(Srcs srcs, int p, int64_t n, int64_t chunk, int start, int64_t off, int mixed,
            typename St<SD>::T* __restrict__ dst, int vec_ok) {
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
-  auto r0_of = [&](int64_t e) -> int {
+  auto r0_of = [&](int64_t e) -> int {  // e + off: the element's index in the whole ring buffer
     if (!mixed) return 0;
-    const int64_t c = chunk > 0 ? e / chunk : 0;
+    const int64_t c = chunk > 0 ? (e + off) / chunk : 0;
     return (int)((start + c) % p);
   };
   auto one = [&](int64_t e) {
@@ -193,10 +194,10 @@ __global__ void __launch_bounds__(256)
   for (int64_t e = done + i0; e < n; e += stride) one(e);
 }
 
-static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int start, int storage,
-                         int compute, int mixed, void* dst, void* stream) {
+static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int start, int64_t off,
+                         int storage, int compute, int mixed, void* dst, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (p < 1 || p > TV_MAX_RANKS || n < 0 || start < 0 || chunk < 0)
+  if (p < 1 || p > TV_MAX_RANKS || n < 0 || start < 0 || chunk < 0 || off < 0)
     return set_error(TV_ECOLL, "tv_rank_fold: bad rank count / length / chunk");
   if (n == 0) return TV_OK;
   int v = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
@@ -204,11 +205,11 @@ static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int sta
   const int sb = dtype_bytes(storage);
   const unsigned g = grid_1d(v && sb > 0 ? (n * sb + 15) / 16 : n, 256);
   switch (mode_id(storage, compute)) {
-    case MODE_F64: k_fold<TV_F64, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (double*)dst, v); break;
-    case MODE_F32: k_fold<TV_F32, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (float*)dst, v); break;
-    case MODE_F32F64: k_fold<TV_F32, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (float*)dst, v); break;
-    case MODE_F16F32: k_fold<TV_F16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (uint16_t*)dst, v); break;
-    case MODE_BF16F32: k_fold<TV_BF16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, mixed, (uint16_t*)dst, v); break;
+    case MODE_F64: k_fold<TV_F64, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, off, mixed, (double*)dst, v); break;
+    case MODE_F32: k_fold<TV_F32, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, off, mixed, (float*)dst, v); break;
+    case MODE_F32F64: k_fold<TV_F32, double><<<g, 256, 0, st>>>(s, p, n, chunk, start, off, mixed, (float*)dst, v); break;
+    case MODE_F16F32: k_fold<TV_F16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, off, mixed, (uint16_t*)dst, v); break;
+    case MODE_BF16F32: k_fold<TV_BF16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, off, mixed, (uint16_t*)dst, v); break;
     default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
   }
   return check_launch("tv_rank_fold");
@@ -413,7 +414,7 @@ extern "C" int tv_rank_fold(const void* const* srcs, int p, int64_t n, int64_t c
     if (!srcs[r] && n > 0) return set_error(TV_ECOLL, "tv_rank_fold: null source");
     s.p[r] = srcs[r];
   }
-  return fold_dispatch(s, p, n, chunk, start, storage, compute, mixed, dst, stream);
+  return fold_dispatch(s, p, n, chunk, start, 0, storage, compute, mixed, dst, stream);
 }
 
 extern "C" int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64_t n,
@@ -427,7 +428,22 @@ extern "C" int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, i
   Srcs s{};
   for (int r = 0; r < p; ++r)
     s.p[r] = static_cast<const char*>(src) + (size_t)r * (size_t)src_stride_elems * (size_t)sb;
-  return fold_dispatch(s, p, n, chunk, start, storage, compute, mixed, dst, stream);
+  return fold_dispatch(s, p, n, chunk, start, 0, storage, compute, mixed, dst, stream);
+}
+
+extern "C" int tv_rank_fold_range(const void* src, int64_t src_stride_elems, int p, int64_t n,
+                                  int64_t ring_chunk, int64_t offset, int storage, int compute,
+                                  int mixed, void* dst, void* stream) {
+  using namespace tv;
+  if (!src || p < 1 || p > TV_MAX_RANKS || src_stride_elems < n || offset < 0 ||
+      (mixed && ring_chunk < 1))
+    return set_error(TV_ECOLL, "tv_rank_fold_range: bad arguments");
+  const int sb = dtype_bytes(storage);
+  if (sb <= 0) return set_error(TV_EMODE, "tv_rank_fold_range: bad storage dtype");
+  Srcs s{};
+  for (int r = 0; r < p; ++r)
+    s.p[r] = static_cast<const char*>(src) + (size_t)r * (size_t)src_stride_elems * (size_t)sb;
+  return fold_dispatch(s, p, n, ring_chunk, 0, offset, storage, compute, mixed, dst, stream);
 }
 
 extern "C" int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t chunk, int dtype,

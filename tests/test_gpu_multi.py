@@ -39,7 +39,7 @@ def _worker(rank, world, port, q):
         import tenvec_oracle as O
         import paper_2501_03121_b200 as tv
 
-        group = tv.RankGroup()
+        group = tv.RankGroup(algo="exact")
         # dtvc on a device-generated 5-mode tensor: every k, split on / off k
         shape = (6, 8, world * 3, 5, 4)
         full = O.fill_values(shape, "hash", seed=4).reshape(shape)
@@ -79,6 +79,25 @@ def _worker(rank, world, port, q):
         want = torch.arange(1, 300_003, dtype=torch.float32) * sum(r + 1 for r in range(world))
         p2p.all_reduce_sum(rank, rag)
         ok.append(("f32", "ragged-p2p", 0, bool(torch.equal(rag.cpu(), want))))
+        # the split-mode contraction fused with its reduction over peer memory
+        # (algo="fused"): slab-range owners (u >= p), column-range owners
+        # (u == 1, unaligned columns), the fallback (1 < u < p), every mode
+        fused = tv.RankGroup(algo="fused")
+        for fshape, s in (((5, 6, world * 3, 7), 2), ((world * 4, 30, 7), 0), ((3, world * 2, 50), 1),
+                          ((2, world * 3, 40), 1)):
+            fullf = O.fill_values(fshape, "hash", seed=8).reshape(fshape)
+            for name in ("f64", "f32", "bf16f32", "f16f32"):
+                mode = tv.MODES[name]
+                hostf = O.demote(fullf.reshape(-1), name).reshape(fshape)
+                x = O.demote((np.arange(fshape[s]) % 7) + 1.0, name).copy()
+                parts, ranges = O.split(hostf, s, world)
+                _, outs, _ = O.dtvc(parts, ranges, s, x, s, name)
+                dt = tv.distribute_generated(tv.Shape(fshape), s, world, mode, fill="hash", seed=8, group=fused)
+                for _ in range(2):  # twice: the symmetric slots are reused
+                    got = tv.dtvc(dt, x, s).parts[0].to_numpy()
+                ok.append((name, "fused", fshape, bool(np.array_equal(_bits(got), _bits(outs[0].reshape(-1))))))
+                sweep = tv.dtvc_sweep(dt, [O.demote(np.ones(n), name).copy() for n in fshape])
+                ok.append((name, "fused-sweep", fshape, sweep[s].parts[0].size == outs[0].size))
         # dhopm3 over NCCL equals the in-process oracle run
         hshape = (world * 4, 10, 9)
         vals = np.random.default_rng(7).standard_normal(hshape)
