@@ -20,6 +20,7 @@ def main() -> int:
     ap.add_argument("--mode", default="f64")
     ap.add_argument("--k", type=int, required=True)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--naive", action="store_true", help="the tv_tvc_naive cross-check kernel instead")
     args = ap.parse_args()
     import torch
 
@@ -33,7 +34,10 @@ def main() -> int:
         torch.full((n,), 0x3F80, dtype=torch.int16, device="cuda").view(torch.uint16)
     out = torch.empty(t.size // n, dtype=mode.torch_storage, device="cuda")
     for _ in range(args.reps):
-        tv.tvc_native(t, x, args.k, out=out)
+        if args.naive:
+            tv.tvc_looped_oracle(t, x, args.k)
+        else:
+            tv.tvc_native(t, x, args.k, out=out)
     torch.cuda.synchronize()
     print(args.shape, args.mode, args.k, tv.tvc_regime(t, args.k))
     return 0

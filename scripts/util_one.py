@@ -35,7 +35,28 @@ def main() -> int:
         tv.normalize(v)
         # device fill of a 2 GB slab
         tv.distribute_generated(tv.Shape((1024, 1024, 256)), 0, 1, tv.F64, fill="hash")
-        del bufs, bb, src
+        # fused last contraction + normalize of a dHOPM3 iteration (2000 x 2000 fp64)
+        w = tv.Tensor(tv.Shape((2000, 2000)), torch.ones(4_000_000, dtype=torch.float64, device="cuda"), tv.F64)
+        slot = torch.empty(1, dtype=torch.float64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        tv.tvc_normalize_async(w, torch.ones(2000, dtype=torch.float64, device="cuda"), 1,
+                               torch.empty(2000, dtype=torch.float64, device="cuda"), slot, None, cnt)
+        # axpby over 64 Mi fp32 (kernels.py:191-231)
+        xa = torch.ones(n, dtype=torch.float32, device="cuda")
+        ya = torch.ones(n, dtype=torch.float32, device="cuda")
+        tv.axpby(2.0, xa, 0.5, ya, mode=tv.F32)
+        # select-gather of 8 ranges (the peer-memory allreduce's gather phase)
+        import ctypes
+        from paper_2501_03121_b200 import _lib
+        srcs = [torch.full((n,), float(r), dtype=torch.float32, device="cuda") for r in range(8)]
+        arr = (ctypes.c_void_p * 8)(*[b.data_ptr() for b in srcs])
+        dst = torch.empty(n, dtype=torch.float32, device="cuda")
+        _lib.check(_lib.load().tv_rank_select(arr, 8, n, n // 8, _lib.TV_F32, dst.data_ptr(), _lib.stream_ptr()))
+        # read-only roofline probe over 2 GB
+        sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+        big = torch.ones(1 << 31, dtype=torch.uint8, device="cuda")
+        _lib.check(_lib.load().tv_read_stream(big.data_ptr(), big.numel(), sink.data_ptr(), _lib.stream_ptr()))
+        del bufs, bb, src, w, xa, ya, srcs, dst, big
     torch.cuda.synchronize()
     print("util kernels ok")
     return 0
