@@ -96,7 +96,8 @@ int tv_tvc_normalize(const void* A, int storage, int compute, int64_t u, int64_t
 /* Which kernel regime tv_tvc would pick for this view: 1 rows, 2 short rows,
  * 3 columns, 4 narrow slabs, and their unaligned (scalar-load) forms 5 rows,
  * 6 columns, 7 slabs, 8 slabs staged through shared memory by TMA bulk
- * copies, 9 flat narrow slabs, 10 flat short rows (0 is the naive kernel,
+ * copies, 9 flat narrow slabs, 10 flat short rows, 11 larger unaligned slabs
+ * as TMA row-run tiles (0 is the naive kernel,
  * tv_tvc_naive only); -1 on invalid arguments. */
 int tv_tvc_regime(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
 

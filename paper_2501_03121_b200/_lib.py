@@ -21,7 +21,7 @@ TV_FILL_ONES, TV_FILL_RAMP, TV_FILL_HASH = 0, 1, 2
 TV_MAX_RANKS = 64
 REGIMES = {0: "naive", 1: "rows", 2: "rows_short", 3: "cols", 4: "slabs", 5: "rows_u", 6: "cols_u",
            7: "slabs_u", 8: "staged", 9: "flat",
-           10: "flat_rows"}
+           10: "flat_rows", 11: "staged_long"}
 
 _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p

@@ -18,9 +18,10 @@ enum {
   REG_ROWS_U = 5,  // unaligned forms: scalar, lane-interleaved loads
   REG_COLS_U = 6,
   REG_SLABS_U = 7,
-  REG_STAGED = 8,  // small slabs staged through shared memory (cp.async)
+  REG_STAGED = 8,  // slabs that fit a tile, staged through shared memory (TMA bulk)
   REG_FLAT = 9,      // narrow aligned slabs streamed as flat warp runs
-  REG_FLAT_ROWS = 10  // short aligned rows streamed as flat warp runs
+  REG_FLAT_ROWS = 10,   // short aligned rows streamed as flat warp runs
+  REG_STAGED_LONG = 11  // larger unaligned slabs: row-run tiles by TMA, sums kept across tiles
 };
 
 // the five valid (storage, compute) pairs of precision.py:81-87

@@ -813,6 +813,136 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------- STAGED_LONG ----
+// Slabs larger than a tile with at most kLongCols columns (unaligned wide
+// views, e.g. paper d = 7 k = 4: 19 x 361 fp64 slabs of 55 KB).  A slab's
+// rows are contiguous, so a run of R rows of one slab is ONE contiguous byte
+// range: each tile is a single TMA bulk copy (as in STAGED), a CTA walks the
+// tiles of its slabs in order, and thread (gi, c) keeps the partial sums of
+// columns c, c + per, ... (M of them) in registers across the slab's tiles;
+// the G row groups (narrow slabs) fold through shared memory at slab end.
+constexpr int kLongCols = 16 * kThreads;
+
+template <int SD, typename C, int M>
+__global__ void __launch_bounds__(kThreads)
+    k_staged_long(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+                  typename St<SD>::T* __restrict__ y, int64_t u, int nk, int v, int tps, int G,
+                  int sbytes, C alpha, C beta, int has_beta) {
+  using T = typename St<SD>::T;
+  constexpr int SB = sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int xs_pad = (nk * (int)sizeof(C) + 15) / 16 * 16;
+  C* xs = reinterpret_cast<C*>(smem_raw);
+  unsigned char* const stage0 = smem_raw + xs_pad;
+  C* red = reinterpret_cast<C*>(smem_raw + xs_pad + 2 * (sbytes + 16));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + xs_pad + 2 * (sbytes + 16) +
+                                               (kThreads * sizeof(C) + 7) / 8 * 8);
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) xs[i] = promote<SD, C>(x[i]);
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const unsigned char* gbase = reinterpret_cast<const unsigned char*>(A);
+  const int64_t row_bytes = (int64_t)v * SB;
+  const int64_t total_bytes = u * nk * row_bytes;
+  const int64_t bulk_end = total_bytes & ~(int64_t)15;
+  const int64_t my_slabs = blockIdx.x < u ? (u - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t my_tiles = my_slabs * tps;
+  // a slab's nk rows over its tps tiles: the first (nk % tps) tiles take one
+  // row more.  Cursors advance incrementally (no divisions per tile): (slab,
+  // tile q, first row j0) of the tile being summed and, on thread 0, of the
+  // tile being fetched.
+  const int rbase = nk / tps, rrem = nk % tps;
+  const int per = kThreads / G;
+  const int gi = threadIdx.x / per;
+  const int c = threadIdx.x - gi * per;
+  C acc[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m] = C(0);
+
+  int64_t f_slab = blockIdx.x;  // fetch cursor (thread 0)
+  int f_q = 0, f_j0 = 0;
+  auto fetch = [&](int k) {
+    const int f_j1 = f_j0 + rbase + (f_q < rrem ? 1 : 0);
+    const int64_t b0 = (f_slab * nk + f_j0) * row_bytes;
+    const int64_t a0 = b0 & ~(int64_t)15;
+    const int64_t e16 = (b0 + (f_j1 - f_j0) * row_bytes + 15) & ~(int64_t)15;
+    const int64_t a1 = e16 < bulk_end ? e16 : bulk_end;
+    const unsigned nb = a1 > a0 ? (unsigned)(a1 - a0) : 0u;
+    unsigned char* dst = stage0 + k * (sbytes + 16);
+    mbar_expect_tx(&bars[k], nb);
+    if (nb) bulk_g2s(dst, gbase + a0, nb, &bars[k]);
+    if (++f_q == tps) {
+      f_q = 0;
+      f_j0 = 0;
+      f_slab += gridDim.x;
+    } else {
+      f_j0 = f_j1;
+    }
+  };
+  if (threadIdx.x == 0 && my_tiles > 0) fetch(0);
+
+  int64_t slab = blockIdx.x;  // sum cursor (every thread)
+  int q = 0, j0 = 0;
+  for (int64_t t = 0; t < my_tiles; ++t) {
+    const int k = (int)(t & 1);
+    if (threadIdx.x == 0 && t + 1 < my_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      fetch(k ^ 1);
+    }
+    const int j1 = j0 + rbase + (q < rrem ? 1 : 0);
+    const int64_t b0 = (slab * nk + j0) * row_bytes;
+    unsigned char* const sp = stage0 + k * (sbytes + 16);
+    mbar_wait(&bars[k], (unsigned)(t >> 1) & 1u);
+    if (b0 + (j1 - j0) * row_bytes > bulk_end) {  // block-uniform: the buffer's ragged end
+      const int64_t a0 = b0 & ~(int64_t)15;
+      for (int64_t b = (bulk_end > a0 ? bulk_end : a0) + threadIdx.x; b < total_bytes; b += blockDim.x)
+        sp[b - a0] = gbase[b];
+      __syncthreads();
+    }
+    const T* tile = reinterpret_cast<const T*>(sp + (b0 & 15));
+    if (gi < G) {
+      for (int r = gi; r < j1 - j0; r += G) {
+        const T* rp = tile + r * v + c;
+        const C xj = xs[j0 + r];
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+          if (c + m * per < v) acc[m] = fma(promote<SD, C>(rp[m * per]), xj, acc[m]);
+      }
+    }
+    if (j1 == nk) {  // slab done: fold the row groups (M == 1 then), write its v outputs
+      if (G > 1) {
+        red[threadIdx.x] = acc[0];
+        __syncthreads();
+        if (gi == 0 && c < v)
+          for (int g2 = 1; g2 < G; ++g2) acc[0] += red[g2 * per + c];
+      }
+      if (gi == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          if (c + m * per < v) {
+            const int64_t o = slab * v + c + m * per;
+            y[o] = epilogue<SD, C>(acc[m], alpha, beta, has_beta != 0, y + o);
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < M; ++m) acc[m] = C(0);
+    }
+    if (++q == tps) {
+      q = 0;
+      j0 = 0;
+      slab += gridDim.x;
+    } else {
+      j0 = j1;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------- TVC + NORMALIZE ----
 // The last contraction of a dHOPM3 iteration (the carried 2-mode tensor
 // contracted to the iteration's vector, hopm.py:295-319) with the vector
@@ -1003,6 +1133,11 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   const bool al_cols = base_al && su_al && (sk * sb) % 16 == 0 && v % VEC == 0;
   const int stb = stage_bytes();
   const bool stageable = base_al && contiguous && u > 1 && nk * v * sb + 16 <= stb;
+  // STAGED_LONG: >= 8 slabs per co-resident CTA (2 per SM) keeps the tail
+  // short; rows of >= kThreads columns (narrower ones leave threads idle and
+  // make long serial column sums: 175 columns measured 4.6-5.0 vs COLS_U 5.8)
+  const bool long_ok = base_al && contiguous && v >= kThreads && v <= kLongCols && v * sb <= stb &&
+                       nk < (1LL << 31) && u >= 16LL * sm_count() && nk * v * sb + 16 > stb;
   // FLAT: aligned narrow contiguous slabs whose width's odd part is 1 or 3
   // and gcd(32, width) >= 2 (C3 / C4 widths 24, 12, 6 vectors; width 3 folds
   // 32 lanes per column and measured slower than SLABS), slabs of at least
@@ -1026,7 +1161,9 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
                     (forced == REG_SLABS && v > 1 && al_cols && v / VEC < 32) ||
                     (forced == REG_COLS_U && v > 1) || (forced == REG_SLABS_U && v > 1 && v < 32) ||
                     (forced == REG_STAGED && stageable) || (forced == REG_FLAT && flat_ok) ||
-                    (forced == REG_FLAT_ROWS && flat_rows_ok);
+                    (forced == REG_FLAT_ROWS && flat_rows_ok) ||
+                    (forced == REG_STAGED_LONG && base_al && contiguous && v > 1 && v <= kLongCols &&
+                     v * sb <= stb && u > 1);
     if (ok) return forced;
   }
   // measured on B200 (profiles/r01_regime_ab.txt): aligned views always stream
@@ -1053,6 +1190,8 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   if (al_cols && stageable && nk <= 32 && nk * v * sb <= stb / 2) return REG_STAGED;
   if (al_cols) return (v / VEC >= 32) ? REG_COLS : (flat_ok ? REG_FLAT : REG_SLABS);
   if (stageable) return REG_STAGED;  // any unaligned slab that fits one tile
+  // larger unaligned slabs of <= kLongCols columns, many of them: row-run tiles
+  if (long_ok) return REG_STAGED_LONG;
   return v >= 32 ? REG_COLS_U : REG_SLABS_U;
 }
 
@@ -1159,6 +1298,33 @@ static void launch_staged(const void* A, const void* x, void* y, int64_t u, int6
   }
 }
 
+template <int SD, typename C>
+static void launch_staged_long(const void* A, const void* x, void* y, int64_t u, int64_t nk,
+                               int64_t v, C al, C be, int hb, cudaStream_t st) {
+  using T = typename St<SD>::T;
+  const int sbytes = stage_bytes();
+  const int64_t row_bytes = v * (int64_t)sizeof(T);
+  const int64_t rmax = std::max<int64_t>(1, sbytes / row_bytes);
+  const int tps = (int)cdiv(nk, rmax);  // tiles per slab
+  const int R = (int)cdiv(nk, tps);
+  const int G = v < kThreads ? (int)std::max<int64_t>(1, std::min<int64_t>(kThreads / v, R)) : 1;
+  const int M = (int)cdiv(v, kThreads / G);
+  const size_t smem = (size_t)cdiv(nk * (int64_t)sizeof(C), 16) * 16 + 2 * (sbytes + 16) +
+                      (kThreads * sizeof(C) + 7) / 8 * 8 + 2 * sizeof(uint64_t);
+  const int per_sm = std::max(1, std::min(8, (int)(228 * 1024 / (smem + 1024))));
+  const unsigned grid = (unsigned)std::min<int64_t>(u, (int64_t)per_sm * sm_count());
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, tps, G, sbytes,
+                                       al, be, hb);
+  };
+  if (M <= 1) go(k_staged_long<SD, C, 1>);
+  else if (M <= 2) go(k_staged_long<SD, C, 2>);
+  else if (M <= 4) go(k_staged_long<SD, C, 4>);
+  else if (M <= 8) go(k_staged_long<SD, C, 8>);
+  else go(k_staged_long<SD, C, 16>);
+}
+
 template <int SD, typename C, bool AL>
 static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t v,
                        int64_t su, int64_t sk, C al, C be, int hb, cudaStream_t st) {
@@ -1203,6 +1369,9 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       break;
     case REG_STAGED:
       launch_staged<SD, C>(A, x, y, u, nk, v, al, be, hb, st);
+      break;
+    case REG_STAGED_LONG:
+      launch_staged_long<SD, C>(A, x, y, u, nk, v, al, be, hb, st);
       break;
     case REG_ROWS_SHORT: {
       constexpr int UNR = 4;

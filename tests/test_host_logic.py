@@ -187,6 +187,9 @@ def test_library_argument_validation_without_gpu():
     assert lib.tv_tvc_regime(p, 0, 1000, 131, 1) == 8      # odd fp64 rows <= 2 KB -> staged
     assert lib.tv_tvc_regime(p, 0, 1000, 301, 1) == 5      # odd fp64 long rows -> scalar rows
     assert lib.tv_tvc_regime(p, 0, 9, 979, 979) == 6       # odd fp64 columns -> scalar columns
+    assert lib.tv_tvc_regime(p, 0, 130321, 19, 361) == 11  # many 55 KB unaligned slabs -> row-run tiles
+    assert lib.tv_tvc_regime(p, 0, 30625, 175, 175) == 6   # rows under 256 columns -> scalar columns
+    assert lib.tv_tvc_regime(p, 0, 979, 979, 979) == 6     # too few slabs to balance -> scalar columns
     # the diagnostic override pins a regime only where the view can take it
     prev = lib.tv_set_regime_override(1)
     try:
