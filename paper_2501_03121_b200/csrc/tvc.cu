@@ -913,12 +913,16 @@ __global__ void __launch_bounds__(kThreads)
           if (c + m * per < v) acc[m] = fma(promote<SD, C>(rp[m * per]), xj, acc[m]);
       }
     }
-    if (j1 == nk) {  // slab done: fold the row groups (M == 1 then), write its v outputs
+    if (j1 == nk) {  // slab done: fold the row groups, write its v outputs
       if (G > 1) {
-        red[threadIdx.x] = acc[0];
-        __syncthreads();
-        if (gi == 0 && c < v)
-          for (int g2 = 1; g2 < G; ++g2) acc[0] += red[g2 * per + c];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          red[threadIdx.x] = acc[m];
+          __syncthreads();
+          if (gi == 0 && c + m * per < v)
+            for (int g2 = 1; g2 < G; ++g2) acc[m] += red[g2 * per + c];
+          __syncthreads();
+        }
       }
       if (gi == 0) {
 #pragma unroll
@@ -1134,10 +1138,14 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   const int stb = stage_bytes();
   const bool stageable = base_al && contiguous && u > 1 && nk * v * sb + 16 <= stb;
   // STAGED_LONG: >= 8 slabs per co-resident CTA (2 per SM) keeps the tail
-  // short; rows of >= kThreads columns (narrower ones leave threads idle and
-  // make long serial column sums: 175 columns measured 4.6-5.0 vs COLS_U 5.8)
-  const bool long_ok = base_al && contiguous && v >= kThreads && v <= kLongCols && v * sb <= stb &&
-                       nk < (1LL << 31) && u >= 16LL * sm_count() && nk * v * sb + 16 > stb;
+  // short; rows of > kThreads / 2 columns (narrower ones make long serial
+  // column sums).  Measured: paper d = 4 k = 2 (175 columns) 6.8 vs COLS_U
+  // 5.8 TB/s; on aligned views it beats COLS only for short columns of
+  // fp32/fp64 (n_k <= 128: +1-2 %; n_k = 2048 or bf16 lose)
+  const bool long_ok = base_al && contiguous && v > kThreads / 2 && v <= kLongCols &&
+                       v * sb <= stb && nk < (1LL << 31) && u >= 16LL * sm_count() &&
+                       nk * v * sb + 16 > stb;
+  const bool long_al_ok = long_ok && al_cols && nk <= 128 && sb >= 4 && v >= kThreads;
   // FLAT: aligned narrow contiguous slabs whose width's odd part is 1 or 3
   // and gcd(32, width) >= 2 (C3 / C4 widths 24, 12, 6 vectors; width 3 folds
   // 32 lanes per column and measured slower than SLABS), slabs of at least
@@ -1188,6 +1196,7 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // small aligned slabs with short columns (n_k <= 32) leave COLS/SLABS warps
   // too little work per slab: staged tiles win there (paper d = 9, 10 tensors)
   if (al_cols && stageable && nk <= 32 && nk * v * sb <= stb / 2) return REG_STAGED;
+  if (long_al_ok) return REG_STAGED_LONG;
   if (al_cols) return (v / VEC >= 32) ? REG_COLS : (flat_ok ? REG_FLAT : REG_SLABS);
   if (stageable) return REG_STAGED;  // any unaligned slab that fits one tile
   // larger unaligned slabs of <= kLongCols columns, many of them: row-run tiles
@@ -1307,7 +1316,10 @@ static void launch_staged_long(const void* A, const void* x, void* y, int64_t u,
   const int64_t rmax = std::max<int64_t>(1, sbytes / row_bytes);
   const int tps = (int)cdiv(nk, rmax);  // tiles per slab
   const int R = (int)cdiv(nk, tps);
-  const int G = v < kThreads ? (int)std::max<int64_t>(1, std::min<int64_t>(kThreads / v, R)) : 1;
+  // row groups: all threads busy (two groups of 128 columns for 128 < v < 256)
+  const int G = v >= kThreads ? 1
+                : v > kThreads / 2 ? 2
+                                   : (int)std::max<int64_t>(1, std::min<int64_t>({kThreads / v, R, 32}));
   const int M = (int)cdiv(v, kThreads / G);
   const size_t smem = (size_t)cdiv(nk * (int64_t)sizeof(C), 16) * 16 + 2 * (sbytes + 16) +
                       (kThreads * sizeof(C) + 7) / 8 * 8 + 2 * sizeof(uint64_t);

@@ -188,7 +188,10 @@ def test_library_argument_validation_without_gpu():
     assert lib.tv_tvc_regime(p, 0, 1000, 301, 1) == 5      # odd fp64 long rows -> scalar rows
     assert lib.tv_tvc_regime(p, 0, 9, 979, 979) == 6       # odd fp64 columns -> scalar columns
     assert lib.tv_tvc_regime(p, 0, 130321, 19, 361) == 11  # many 55 KB unaligned slabs -> row-run tiles
-    assert lib.tv_tvc_regime(p, 0, 30625, 175, 175) == 6   # rows under 256 columns -> scalar columns
+    assert lib.tv_tvc_regime(p, 0, 30625, 175, 175) == 11  # 175-column slabs: two row groups
+    assert lib.tv_tvc_regime(p, 0, 30625, 175, 97) == 6    # narrower -> scalar columns
+    assert lib.tv_tvc_regime(p, 0, 100000, 10, 1000) == 11  # aligned short columns -> row-run tiles
+    assert lib.tv_tvc_regime(p, 0, 2048, 2048, 4096) == 3  # aligned long columns stay COLS
     assert lib.tv_tvc_regime(p, 0, 979, 979, 979) == 6     # too few slabs to balance -> scalar columns
     # the diagnostic override pins a regime only where the view can take it
     prev = lib.tv_set_regime_override(1)
