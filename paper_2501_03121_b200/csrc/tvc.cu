@@ -788,8 +788,18 @@ __global__ void __launch_bounds__(kThreads)
             acc[0] = fma(promote<SD, C>(rp[j]), xs[j], acc[0]);
           }
         } else {
+          // four interleaved partial sums: the shared-memory loads of four
+          // rows are in flight together instead of one serial FMA chain
+          // (C3 p = 8 k = 3: 48 rows per thread)
           const T* sp = t + s * L + l;
-          for (int j = gi; j < nk; j += G) acc[0] = fma(promote<SD, C>(sp[j * v]), xs[j], acc[0]);
+          C a4[4] = {C(0), C(0), C(0), C(0)};
+          int j = gi;
+          for (; j + 3 * G < nk; j += 4 * G) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a4[q] = fma(promote<SD, C>(sp[(j + q * G) * v]), xs[j + q * G], a4[q]);
+          }
+          for (; j < nk; j += G) a4[0] = fma(promote<SD, C>(sp[j * v]), xs[j], a4[0]);
+          acc[0] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         }
       }
       C sum = acc[0];
@@ -1197,7 +1207,10 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // too little work per slab: staged tiles win there (paper d = 9, 10 tensors)
   if (al_cols && stageable && nk <= 32 && nk * v * sb <= stb / 2) return REG_STAGED;
   if (long_al_ok) return REG_STAGED_LONG;
-  if (al_cols) return (v / VEC >= 32) ? REG_COLS : (flat_ok ? REG_FLAT : REG_SLABS);
+  // narrow aligned slabs FLAT cannot fold (odd part of the width 5, 7, ...,
+  // or width 3 vectors): staged tiles when a slab fits one (C3 p = 8 k = 3,
+  // 3-vector slabs: 6.8 vs SLABS 5.8 TB/s, profiles/r01_staged_ab/)
+  if (al_cols) return (v / VEC >= 32) ? REG_COLS : (flat_ok ? REG_FLAT : (stageable ? REG_STAGED : REG_SLABS));
   if (stageable) return REG_STAGED;  // any unaligned slab that fits one tile
   // larger unaligned slabs of <= kLongCols columns, many of them: row-run tiles
   if (long_ok) return REG_STAGED_LONG;

@@ -141,7 +141,8 @@ NATURAL = {((300, 96), 1): "staged", ((96, 96, 12), 2): "staged", ((700, 20), 1)
            ((333, 28), 1): "staged", ((77, 24), 1): "staged", ((5000, 8), 1): "staged",
            ((4, 300, 21), 1): "staged", ((61, 130, 1), 1): "staged", ((77, 330), 1): "staged",
            ((7, 40, 363), 1): "cols_u", ((5, 41, 363), 1): "cols_u", ((9, 300, 50), 1): "cols_u",
-           ((3, 5, 4000), 1): "cols", ((2, 700, 33), 1): "cols_u"}
+           ((3, 5, 4000), 1): "cols", ((2, 700, 33), 1): "cols_u", ((96, 96, 12), 1): "staged",
+           ((3, 200, 20), 1): "staged"}
 
 
 @pytest.fixture

@@ -177,11 +177,13 @@ def test_library_argument_validation_without_gpu():
     assert lib.tv_tvc_regime(p, 1, 1, 12, 1) == 10         # one 3-vector row -> flat rows
     assert lib.tv_tvc_regime(p, 1, 1000, 160, 1) == 1      # aligned longer rows stay rows
     assert lib.tv_tvc_regime(p, 1, 1, 2048, 4096) == 3     # columns
-    assert lib.tv_tvc_regime(p, 1, 1000, 96, 12) == 4      # small aligned slabs
+    assert lib.tv_tvc_regime(p, 1, 1000, 96, 12) == 8      # small aligned 3-vector slabs -> staged
+    assert lib.tv_tvc_regime(p, 1, 1000, 4000, 12) == 4    # larger ones -> slabs
     assert lib.tv_tvc_regime(p, 1, 1000, 13, 1) == 8       # unaligned short rows -> staged
     assert lib.tv_tvc_regime(p, 0, 1000, 13, 13) == 8      # unaligned small slabs -> staged
     assert lib.tv_tvc_regime(p, 1, 1000, 200, 48) == 9     # width 12 vectors -> flat
-    assert lib.tv_tvc_regime(p, 1, 1000, 200, 20) == 4     # width 5 -> slabs
+    assert lib.tv_tvc_regime(p, 1, 1000, 200, 20) == 8     # width 5, fits a tile -> staged
+    assert lib.tv_tvc_regime(p, 1, 1000, 4000, 20) == 4    # width 5 -> slabs
     assert lib.tv_tvc_regime(p + 4, 1, 1000, 96, 12) == 7  # misaligned -> scalar slabs
     assert lib.tv_tvc_regime(p, 0, 1000, 13, 1) == 8       # odd fp64 rows -> staged
     assert lib.tv_tvc_regime(p, 0, 1000, 131, 1) == 8      # odd fp64 rows <= 2 KB -> staged
