@@ -385,3 +385,13 @@ def test_classical_counters_equal_closed_forms(tv):
                 for r in range(p):
                     for j in range(d):
                         assert res.iteration_touched[r][j] == S.m_par(d, 8, p, s, j)[0], (d, p, s, r, j)
+
+
+def test_dtvc_sweep_on_result_reports_every_mode(tv):
+    dt = tv.distribute_generated(tv.Shape((6, 7, 8)), 0, 1, tv.F64, fill="hash", seed=2)
+    xs = [np.ones(n) for n in (6, 7, 8)]
+    seen = []
+    res = tv.dtvc_sweep(dt, xs, on_result=lambda k, r: seen.append((k, r)))
+    assert sorted(k for k, _ in seen) == [0, 1, 2]
+    for k, r in seen:
+        assert r is res[k]
