@@ -147,6 +147,16 @@ int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64
                          int64_t chunk, int start, int storage, int compute, int mixed,
                          void* dst, void* stream);
 
+/* The reduction of a dHOPM3 iteration's vector with the normalisation in
+ * the kernel epilogue (hopm.py:320-330: allreduce, then normalize on every
+ * rank): dst = tv_rank_fold_strided(src, stride, p, n, chunk, start = 0)
+ * and, in the same launch (the last CTA to finish), dst <- dst / ||dst||
+ * with tv_normalize's tree; *norm_out / *status_out as tv_normalize.
+ * counter: a device uint32, 0 on entry, left 0. */
+int tv_rank_fold_normalize(const void* src, int64_t src_stride_elems, int p, int64_t n,
+                           int64_t chunk, int storage, int compute, int mixed, void* dst,
+                           double* norm_out, int32_t* status_out, unsigned* counter, void* stream);
+
 /* tv_rank_fold_strided over a RANGE [offset, offset + n) of a ring buffer
  * whose ring chunks have ring_chunk elements (chunk c starts at rank c, the
  * mixed ring of comm.py:103-134; ignored for the exact fold): the owner of a

@@ -42,6 +42,8 @@ SIGNATURES = {
     "tv_normalize": (_int, [_vp, _int, _int, _i64, _vp, _vp, _vp]),
     "tv_rank_fold": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _int, _int, _int, _vp, _vp]),
     "tv_rank_fold_strided": (_int, [_vp, _i64, _int, _i64, _i64, _int, _int, _int, _int, _vp, _vp]),
+    "tv_rank_fold_normalize": (_int, [_vp, _i64, _int, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp,
+                                       _vp]),
     "tv_rank_fold_range": (_int, [_vp, _i64, _int, _i64, _i64, _i64, _int, _int, _int, _vp, _vp]),
     "tv_rank_select": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp]),
     "tv_fill": (_int, [_vp, _int, _int, ctypes.c_uint64, ctypes.POINTER(_i64), _int, _int, _i64, _i64, _vp]),

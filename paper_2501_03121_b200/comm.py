@@ -541,6 +541,37 @@ class RankGroup:
         self._check_rank(rank)
         self._reduce(buf, True, mode, counters)
 
+    def all_reduce_normalize(self, rank: int, buf: torch.Tensor, mode: PrecisionMode, dst: torch.Tensor,
+                             norm_slot: torch.Tensor, status_slot: torch.Tensor | None,
+                             counter: torch.Tensor, counters: list[CommCounters] | None = None) -> bool:
+        """dHOPM3's reduction of an iteration's vector with the normalisation
+        folded into the fold kernel's epilogue (tv_rank_fold_normalize):
+        dst <- normalize(allreduce(buf)) with the same bits as all_reduce_sum
+        (exact or mixed ring order) followed by normalize (hopm.py:320-330);
+        buf is left as it was.  Latency-sized vectors only (the all-gather
+        path); returns False, doing nothing, when the caller must run the
+        unfused sequence."""
+        self._check_rank(rank)
+        p = self.size
+        n = buf.numel()
+        if p == 1 or n == 0 or not buf.is_cuda or self.fold is not device_fold_strided or \
+                (self.algo == "nccl" and not mode.mixed) or n * buf.element_size() * p > SMALL_GATHER_BYTES:
+            return False
+        sizes = [b - a for a, b in ring_chunks(n, p)]
+        counters = self.counters if counters is None else counters
+        for c in counters:
+            c.collective_calls += 1
+        _charge_allreduce_movement(counters, sizes, p)
+        everyone = torch.empty(p * n, dtype=buf.dtype, device=buf.device)
+        self._dist.all_gather_into_tensor(_wire(everyone), _wire(buf.contiguous()), group=self.group)
+        lib = _lib.load()
+        sp = status_slot.data_ptr() if status_slot is not None else None
+        _lib.check(lib.tv_rank_fold_normalize(everyone.data_ptr(), n, p, n, sizes[0], mode.tv_storage,
+                                              mode.tv_compute, int(mode.mixed), dst.data_ptr(),
+                                              norm_slot.data_ptr(), sp, counter.data_ptr(),
+                                              _lib.stream_ptr()), "allreduce + normalize")
+        return True
+
     def raw_all_gather(self, t: torch.Tensor) -> torch.Tensor:
         """Uncounted byte all-gather of equal-length tensors (bookkeeping checks)."""
         src = t.contiguous().view(torch.uint8)

@@ -8,6 +8,7 @@
 //                                         demote(promote + promote) per hop)
 //   tv_fill         bench.py:62-80       (ones / ramp over the GLOBAL index; the
 //                                         counter hash stands in for numpy's rng)
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -147,9 +148,9 @@ __device__ __forceinline__ typename St<SD>::T fold_hop(typename St<SD>::T cur, t
 // vectors of VEC elements when every pointer is aligned; a vector whose
 // elements straddle a ring chunk boundary (different r0) folds per element.
 template <int SD, typename C>
-__global__ void __launch_bounds__(256)
-    k_fold(Srcs srcs, int p, int64_t n, int64_t chunk, int start, int64_t off, int mixed,
-           typename St<SD>::T* __restrict__ dst, int vec_ok) {
+__device__ __forceinline__ void fold_range(const Srcs& srcs, int p, int64_t n, int64_t chunk, int start,
+                                           int64_t off, int mixed, typename St<SD>::T* __restrict__ dst,
+                                           int vec_ok) {
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
   auto r0_of = [&](int64_t e) -> int {  // e + off: the element's index in the whole ring buffer
@@ -192,6 +193,35 @@ __global__ void __launch_bounds__(256)
     done = nv * VEC;
   }
   for (int64_t e = done + i0; e < n; e += stride) one(e);
+}
+
+template <int SD, typename C>
+__global__ void __launch_bounds__(256)
+    k_fold(Srcs srcs, int p, int64_t n, int64_t chunk, int start, int64_t off, int mixed,
+           typename St<SD>::T* __restrict__ dst, int vec_ok) {
+  fold_range<SD, C>(srcs, p, n, chunk, start, off, mixed, dst, vec_ok);
+}
+
+// The fold of a dHOPM3 iteration's reduction with the vector normalisation in
+// its epilogue: CTAs of kNormThreads fold, the last CTA to take a ticket runs
+// tv_normalize's tree over dst (the same bits as tv_rank_fold + tv_normalize)
+// and resets the ticket.
+template <int SD, typename C>
+__global__ void __launch_bounds__(kNormThreads)
+    k_fold_norm(Srcs srcs, int p, int64_t n, int64_t chunk, int mixed, typename St<SD>::T* __restrict__ dst,
+                int vec_ok, double* __restrict__ norm_out, int32_t* __restrict__ status, unsigned* counter) {
+  __shared__ bool last;
+  fold_range<SD, C>(srcs, p, n, chunk, 0, 0, mixed, dst, vec_ok);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  norm_block<SD, C, true>(dst, n, norm_out, status, 1);
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int start, int64_t off,
@@ -415,6 +445,36 @@ extern "C" int tv_rank_fold(const void* const* srcs, int p, int64_t n, int64_t c
     s.p[r] = srcs[r];
   }
   return fold_dispatch(s, p, n, chunk, start, 0, storage, compute, mixed, dst, stream);
+}
+
+extern "C" int tv_rank_fold_normalize(const void* src, int64_t src_stride_elems, int p, int64_t n,
+                                      int64_t chunk, int storage, int compute, int mixed, void* dst,
+                                      double* norm_out, int32_t* status_out, unsigned* counter,
+                                      void* stream) {
+  using namespace tv;
+  if (!src || !dst || !norm_out || !counter || p < 1 || p > TV_MAX_RANKS || n < 1 ||
+      src_stride_elems < n || chunk < 0)
+    return set_error(TV_ECOLL, "tv_rank_fold_normalize: bad arguments");
+  const int sb = dtype_bytes(storage);
+  if (sb <= 0) return set_error(TV_EMODE, "tv_rank_fold_normalize: bad storage dtype");
+  Srcs s{};
+  int v = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  for (int r = 0; r < p; ++r) {
+    s.p[r] = static_cast<const char*>(src) + (size_t)r * (size_t)src_stride_elems * (size_t)sb;
+    v &= (reinterpret_cast<uintptr_t>(s.p[r]) & 15) == 0;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t work = v ? (n * sb + 15) / 16 : n;
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + kNormThreads - 1) / kNormThreads, 296));
+  switch (mode_id(storage, compute)) {
+    case MODE_F64: k_fold_norm<TV_F64, double><<<g, kNormThreads, 0, st>>>(s, p, n, chunk, mixed, (double*)dst, v, norm_out, status_out, counter); break;
+    case MODE_F32: k_fold_norm<TV_F32, float><<<g, kNormThreads, 0, st>>>(s, p, n, chunk, mixed, (float*)dst, v, norm_out, status_out, counter); break;
+    case MODE_F32F64: k_fold_norm<TV_F32, double><<<g, kNormThreads, 0, st>>>(s, p, n, chunk, mixed, (float*)dst, v, norm_out, status_out, counter); break;
+    case MODE_F16F32: k_fold_norm<TV_F16, float><<<g, kNormThreads, 0, st>>>(s, p, n, chunk, mixed, (uint16_t*)dst, v, norm_out, status_out, counter); break;
+    case MODE_BF16F32: k_fold_norm<TV_BF16, float><<<g, kNormThreads, 0, st>>>(s, p, n, chunk, mixed, (uint16_t*)dst, v, norm_out, status_out, counter); break;
+    default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
+  }
+  return check_launch("tv_rank_fold_normalize");
 }
 
 extern "C" int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64_t n,

@@ -98,6 +98,23 @@ def _worker(rank, world, port, q):
                 ok.append((name, "fused", fshape, bool(np.array_equal(_bits(got), _bits(outs[0].reshape(-1))))))
                 sweep = tv.dtvc_sweep(dt, [O.demote(np.ones(n), name).copy() for n in fshape])
                 ok.append((name, "fused-sweep", fshape, sweep[s].parts[0].size == outs[0].size))
+        # the dHOPM3 reduction with the normalisation in the fold's epilogue:
+        # the same bits as all_reduce_sum + normalize
+        for name in ("f64", "f32", "bf16f32", "f16f32"):
+            mode = tv.MODES[name]
+            for n in (384, 4096, 1001):
+                v = torch.from_numpy(O.demote(np.random.default_rng(rank + n).standard_normal(n), name).copy())
+                v = v.cuda() if v.dtype != torch.uint16 else v.view(torch.int16).cuda().view(torch.uint16)
+                ref = v.clone()
+                group.all_reduce_sum_mixed(rank, ref, mode) if mode.mixed else group.all_reduce_sum(rank, ref)
+                ref_norm = tv.normalize(ref, mode=mode)
+                dst = torch.empty_like(v)
+                slot = torch.empty(1, dtype=torch.float64, device="cuda")
+                cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+                okf = group.all_reduce_normalize(rank, v, mode, dst, slot, None, cnt)
+                same = bool(torch.equal(dst.view(torch.uint8) if dst.dtype != torch.uint16 else dst.view(torch.int16),
+                                        ref.view(torch.uint8) if ref.dtype != torch.uint16 else ref.view(torch.int16)))
+                ok.append((name, "fold-normalize", n, okf and same and float(slot.item()) == ref_norm))
         # dhopm3 over NCCL equals the in-process oracle run
         hshape = (world * 4, 10, 9)
         vals = np.random.default_rng(7).standard_normal(hshape)
