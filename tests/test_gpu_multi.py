@@ -98,6 +98,26 @@ def _worker(rank, world, port, q):
                 ok.append((name, "fused", fshape, bool(np.array_equal(_bits(got), _bits(outs[0].reshape(-1))))))
                 sweep = tv.dtvc_sweep(dt, [O.demote(np.ones(n), name).copy() for n in fshape])
                 ok.append((name, "fused-sweep", fshape, sweep[s].parts[0].size == outs[0].size))
+        # on-device assembly over NCCL: disjoint results gathered and repacked,
+        # deferred partial sums gathered and folded (undistribute, hopm.py:76-84)
+        ashape = (5, world * 3, 4, 6)
+        fulla = O.fill_values(ashape, "hash", seed=9).reshape(ashape)
+        for name in ("f64", "f32", "bf16f32"):
+            mode = tv.MODES[name]
+            hosta = O.demote(fulla.reshape(-1), name).reshape(ashape)
+            dt = tv.distribute_generated(tv.Shape(ashape), 1, world, mode, fill="hash", seed=9, group=group)
+            whole = tv.undistribute(dt).to_numpy()
+            ok.append((name, "assemble-input", 0, bool(np.array_equal(_bits(whole), _bits(hosta.reshape(-1))))))
+            for k in (0, 3):
+                x = O.demote((np.arange(ashape[k]) % 4) + 1.0, name).copy()
+                got = tv.undistribute(tv.dtvc(dt, x, k)).to_numpy()
+                want = O.tvc(hosta.reshape(-1), ashape, x, k, name)
+                ok.append((name, "assemble", k, bool(np.array_equal(_bits(got), _bits(want)))))
+            x = O.demote((np.arange(ashape[1]) % 4) + 1.0, name).copy()
+            got = tv.undistribute(tv.dtvc(dt, x, 1, defer=True)).to_numpy()
+            want = O.tvc(hosta.reshape(-1), ashape, x, 1, name)
+            ok.append((name, "assemble-partial", 1,
+                       bool(np.allclose(O.promote(got, name), O.promote(want, name), rtol=1e-2 if name == "bf16f32" else 1e-6))))
         # the dHOPM3 reduction with the normalisation in the fold's epilogue:
         # the same bits as all_reduce_sum + normalize
         for name in ("f64", "f32", "bf16f32", "f16f32"):
