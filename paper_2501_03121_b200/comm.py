@@ -402,6 +402,11 @@ class RankGroup:
         _lib.check(lib.tv_rank_select(srcs, p, n, q, st, buf.data_ptr(), stream), "p2p gather")
         hdl.barrier(channel=0)                      # peers done reading this buffer
 
+    def _owner_streams(self, device) -> tuple:
+        if getattr(self, "_lanes", None) is None:
+            self._lanes = (torch.cuda.Stream(device=device), torch.cuda.Stream(device=device))
+        return self._lanes
+
     def tvc_reduce_fused(self, part, xv: torch.Tensor, k: int, mode: PrecisionMode,
                          counters: list[CommCounters] | None = None,
                          finish_stream: torch.cuda.Stream | None = None) -> torch.Tensor | None:
@@ -447,23 +452,33 @@ class RankGroup:
         _charge_allreduce_movement(counters, [b - a for a, b in ring], p)
         ptrs = [int(ptr) for ptr in hdl.buffer_ptrs]
         lib = _lib.load()
-        stream = _lib.stream_ptr()
         st_, ct_ = mode.tv_storage, mode.tv_compute
         a_ptr = part.buf.data_ptr()
         hdl.barrier(channel=0)  # peers are done with the previous call's slots
+        # the p owner launches alternate over two streams so one launch's tail
+        # overlaps the next one's ramp (each is a full-GPU grid)
+        main = torch.cuda.current_stream()
+        lanes = self._owner_streams(part.buf.device)
+        for ls in lanes:
+            ls.wait_stream(main)
+        xv.record_stream(lanes[0])
+        xv.record_stream(lanes[1])
         for j in range(p):  # own range first, then the peers in ring order
             c = (rank + j) % p
             lo, hi = bounds[c]
             if hi <= lo:
                 continue
             dst = ptrs[c] + rank * slot_bytes
+            ls = _lib.stream_ptr(lanes[j % 2])
             if along_u:
                 rc = lib.tv_tvc(a_ptr + lo * nk * v * sb, st_, ct_, hi - lo, nk, v, xv.data_ptr(),
-                                1.0, 0.0, dst, stream)
+                                1.0, 0.0, dst, ls)
             else:  # u == 1: columns [lo, hi) of the nk x v slab, a strided vecmat
                 rc = lib.tv_getvc(1, a_ptr + lo * sb, st_, ct_, nk, hi - lo, v, xv.data_ptr(),
-                                  1.0, 0.0, dst, stream)
+                                  1.0, 0.0, dst, ls)
             _lib.check(rc, "fused dtvc: contraction into peer memory")
+        for ls in lanes:
+            main.wait_stream(ls)
         out = torch.empty(n, dtype=mode.torch_storage, device=part.buf.device)
         if finish_stream is not None:
             finish_stream.wait_stream(torch.cuda.current_stream())
