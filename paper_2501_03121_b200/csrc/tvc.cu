@@ -1210,6 +1210,9 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // narrow aligned slabs FLAT cannot fold (odd part of the width 5, 7, ...,
   // or width 3 vectors): staged tiles when a slab fits one (C3 p = 8 k = 3,
   // 3-vector slabs: 6.8 vs SLABS 5.8 TB/s, profiles/r01_staged_ab/)
+  // 6-vector slabs (gcd 2: 16 lanes per column fold) stream faster staged
+  // (C3 p = 4 k = 3: 7.0 vs FLAT 6.7 TB/s); wider gcds keep FLAT
+  if (al_cols && flat_ok && gg < 4 && stageable) return REG_STAGED;
   if (al_cols) return (v / VEC >= 32) ? REG_COLS : (flat_ok ? REG_FLAT : (stageable ? REG_STAGED : REG_SLABS));
   if (stageable) return REG_STAGED;  // any unaligned slab that fits one tile
   // larger unaligned slabs of <= kLongCols columns, many of them: row-run tiles
