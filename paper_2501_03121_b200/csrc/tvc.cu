@@ -108,8 +108,22 @@ __global__ void __launch_bounds__(kThreads)
   auto fold_vec = [&](const uint4& raw, int64_t j0, C (&acc)[VEC]) {
     C a[VEC];
     unpack<SD, C>(raw, a);
+    if constexpr (XS && !PEEL) {
+      // aligned rows: the VEC x values of a vector are contiguous 16-byte
+      // aligned words of shared memory -- 16-byte loads, not VEC scalar ones
+      constexpr int NX = VEC * (int)sizeof(C) / 16;
+      union {
+        uint4 u[NX];
+        C c[VEC];
+      } xw;
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) acc[e] = fma(a[e], xv(j0 + e), acc[e]);
+      for (int q = 0; q < NX; ++q) xw.u[q] = reinterpret_cast<const uint4*>(xs + j0)[q];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = fma(a[e], xw.c[e], acc[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = fma(a[e], xv(j0 + e), acc[e]);
+    }
   };
   // head and tail elements of a peeled row (returned, added to acc[0] after)
   auto fold_edges = [&](const T* rp, int64_t h, int64_t nb) -> C {
@@ -1263,6 +1277,11 @@ static void launch_rows_auto(const void* A, const void* x, void* y, int64_t u, i
   constexpr int VEC = VecN<SD>::N;
   const int64_t nunits = std::max<int64_t>(1, nk / VEC);
   int G = pick_row_group(nunits);
+  static const int g_env = [] {  // TENVEC_B200_ROW_G: lanes per row, for A/B runs
+    const char* e = getenv("TENVEC_B200_ROW_G");
+    return e ? atoi(e) : 0;
+  }();
+  if (g_env == 1 || g_env == 2 || g_env == 4 || g_env == 8 || g_env == 16 || g_env == 32) G = g_env;
   const int64_t qpl = cdiv(nunits, G);
   bool lng = qpl > kRowBatch;
   int RS = lng ? 1 : (qpl * 4 <= kRowBatch ? 4 : qpl * 2 <= kRowBatch ? 2 : 1);
