@@ -13,7 +13,11 @@ from pathlib import Path
 
 from .errors import CollectiveError, DeviceError, KernelError, ModeError, NormalizationError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libtenvec_b200.so"
+import os as _os
+
+# TENVEC_B200_LIB: load another build of the library (kernel A/B variants)
+LIB_PATH = Path(_os.environ.get("TENVEC_B200_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libtenvec_b200.so")
 
 # tv_dtype codes
 TV_F64, TV_F32, TV_F16, TV_BF16 = 0, 1, 2, 3

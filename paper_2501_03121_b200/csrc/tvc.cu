@@ -1377,7 +1377,7 @@ static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t
                        int64_t su, int64_t sk, C al, C be, int hb, cudaStream_t st) {
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
-  constexpr int UA_UNR = VEC >= 8 ? 2 : 4;  // scalar loads in flight: UNR * VEC
+  constexpr int UA_UNR = VEC >= 8 ? 2 : 4;  // scalar loads in flight: UNR * VEC (8 measured slower)
   const int64_t stripes = cdiv(v, 32 * VEC);
   const int JR = pick_col_phases(nk, stripes, u);
   const int64_t ntile = cdiv(stripes, kWarps / JR);
