@@ -288,7 +288,10 @@ def test_c1_256_cubed_every_mode_bitwise(tv):
 
 
 @pytest.mark.parametrize("mode_name,shape", [("f64", (1024, 1024, 1024)), ("f32", (96, 96, 96, 96)),
-                                             ("bf16f32", (2048, 2048, 256))])
+                                             ("bf16f32", (2048, 2048, 256)),
+                                             # past 2**32 elements (int64 indexing), and odd
+                                             # extents past 2**31 (unaligned regimes)
+                                             ("f32", (2048, 2048, 1040)), ("f64", (1501, 1499, 1001))])
 def test_large_views_sampled_exact(tv, mode_name, shape):
     """Full-size-style views checked on sampled outputs regenerated from the
     closed-form hash fill (size-independent, exact for integer data)."""
