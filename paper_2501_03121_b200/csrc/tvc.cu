@@ -1387,6 +1387,16 @@ static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t
   const T* xt = (const T*)x;
   T* yt = (T*)y;
   const unsigned b = (unsigned)blocks;
+  // unaligned, fp32/fp64: 3-row batches measured better for 4 row phases
+  // (paper d = 3: 7.1-7.2 vs 6.6-6.8 TB/s) and for n_k <= 16 (d = 8: 6.4 vs
+  // 6.1); 4 elsewhere (d = 2 k = 0 with 8 phases: 5.9 vs 5.1)
+  if (!AL && VEC <= 4 && (JR == 4 || (JR == 1 && nk <= 16))) {
+    if (JR == 4)
+      k_cols<SD, C, 4, 3, false><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb);
+    else
+      k_cols<SD, C, 1, 3, false><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb);
+    return TV_OK;
+  }
   switch (JR) {
     case 1: k_cols<SD, C, 1, AL ? 8 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
     case 2: k_cols<SD, C, 2, AL ? 8 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
