@@ -273,11 +273,12 @@ __global__ void __launch_bounds__(kThreads)
 // rows j = r, r + JR, ... of its stripe.  Aligned: lane owns one 16-byte
 // vector (VEC adjacent columns); unaligned: lane owns VEC columns 32 apart, so
 // each of its scalar loads is part of one contiguous 32-element warp access.
-template <int SD, typename C, int JR, int UNR, bool AL>
+template <int SD, typename C, int JR, int UNR, bool AL, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreads)
     k_cols(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
-           typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t v, int64_t su,
-           int64_t sk, int64_t ntile, C alpha, C beta, int has_beta) {
+           typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk_all, int64_t v, int64_t su,
+           int64_t sk, int64_t ntile, C alpha, C beta, int has_beta, int64_t rpc,
+           C* __restrict__ ws) {
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
   constexpr int CW = kWarps / JR;
@@ -294,6 +295,11 @@ __global__ void __launch_bounds__(kThreads)
     return AL ? (sbase + lane) * VEC + e : sbase * VEC + (int64_t)e * 32 + lane;
   };
   const bool any = AL ? (sbase + lane) * VEC < v : sbase * VEC + lane < v;
+  // row chunk blockIdx.y: rows [jb, nk) (one chunk = the whole column when
+  // gridDim.y == 1); with ws the chunk's partial sums go there, no epilogue
+  // (SPLIT = false compiles the whole-column form: jb = 0, nk = nk_all)
+  const int64_t jb = SPLIT ? (int64_t)blockIdx.y * rpc : 0;
+  const int64_t nk = SPLIT ? (jb + rpc < nk_all ? jb + rpc : nk_all) : nk_all;
   const T* base = A + i * su;
   C acc[VEC];
 #pragma unroll
@@ -301,7 +307,7 @@ __global__ void __launch_bounds__(kThreads)
   if (any) {
     // full batches of UNR rows without predicates (all loads issue back to
     // back), then the remaining rows one at a time
-    int64_t j0 = r;
+    int64_t j0 = jb + r;
     if constexpr (AL) {
       const T* cb = base + (sbase + lane) * VEC;
       auto fold = [&](const uint4& raw, int64_t j) {
@@ -371,13 +377,18 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   }
+  const int64_t wrow = (i * gridDim.y + blockIdx.y) * v;  // partial row in ws
   if constexpr (JR == 1) {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       const int64_t c = col_of(e);
       if (c < v) {
-        const int64_t o = i * v + c;
-        y[o] = epilogue<SD, C>(acc[e], alpha, beta, has_beta != 0, y + o);
+        if (SPLIT && ws != nullptr) {
+          ws[wrow + c] = acc[e];
+        } else {
+          const int64_t o = i * v + c;
+          y[o] = epilogue<SD, C>(acc[e], alpha, beta, has_beta != 0, y + o);
+        }
       }
     }
   } else {
@@ -385,15 +396,19 @@ __global__ void __launch_bounds__(kThreads)
     for (int e = 0; e < VEC; ++e) red[r][stripe][lane][e] = acc[e];
     __syncthreads();
     if (r == 0) {
-      const int64_t jr = nk < JR ? nk : JR;
+      const int64_t jr = nk - jb < JR ? nk - jb : JR;
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         const int64_t c = col_of(e);
         if (c < v) {
           C s = red[0][stripe][lane][e];
           for (int k = 1; k < jr; ++k) s += red[k][stripe][lane][e];
-          const int64_t o = i * v + c;
-          y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+          if (SPLIT && ws != nullptr) {
+            ws[wrow + c] = s;
+          } else {
+            const int64_t o = i * v + c;
+            y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+          }
         }
       }
     }
@@ -572,7 +587,8 @@ template <int SD, typename C, int UNR, bool AL>
 __global__ void __launch_bounds__(kThreads)
     k_slabs(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
             typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int v, int64_t su,
-            int64_t sk, C alpha, C beta, int has_beta) {
+            int64_t sk, C alpha, C beta, int has_beta, int64_t nch, int64_t rpc,
+            C* __restrict__ ws) {
   using U = Unit<SD, C, AL>;
   constexpr int N = U::N;
   __shared__ C red[kWarps][32][N + (sizeof(C) == 8 ? 0 : 1)];
@@ -585,23 +601,27 @@ __global__ void __launch_bounds__(kThreads)
   const bool active = r < R;
   const int64_t warps_total = (int64_t)gridDim.x * kWarps;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + w;
-  for (int64_t i = gw; i < u; i += warps_total) {
+  // a warp unit = (slab i, row chunk ch); nch == 1: whole slabs, no partials
+  for (int64_t unit = gw; unit < u * nch; unit += warps_total) {
+    const int64_t i = unit / nch;
+    const int64_t jb = (unit - i * nch) * rpc;
+    const int64_t je = jb + rpc < nk ? jb + rpc : nk;
     const auto* base = A + i * su + c * N;
     C acc[N];
 #pragma unroll
     for (int e = 0; e < N; ++e) acc[e] = C(0);
     // predicated batches (measured faster here than split full/remainder loops)
-    for (int64_t j0 = r; j0 < nk; j0 += (int64_t)R * UNR) {
+    for (int64_t j0 = jb + r; j0 < je; j0 += (int64_t)R * UNR) {
       typename U::Raw buf[UNR];
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
         const int64_t j = j0 + (int64_t)t * R;
-        if (active && j < nk) buf[t] = U::load(base + j * sk);
+        if (active && j < je) buf[t] = U::load(base + j * sk);
       }
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
         const int64_t j = j0 + (int64_t)t * R;
-        if (active && j < nk) {
+        if (active && j < je) {
           const C xj = promote<SD, C>(__ldg(x + j));
           C a[N];
           U::widen(buf[t], a);
@@ -614,13 +634,17 @@ __global__ void __launch_bounds__(kThreads)
     for (int e = 0; e < N; ++e) red[w][lane][e] = acc[e];
     __syncwarp();
     if (lane < units) {
-      const int64_t rr = nk < R ? nk : R;
+      const int64_t rr = je - jb < R ? je - jb : R;
 #pragma unroll
       for (int e = 0; e < N; ++e) {
         C s = red[w][lane][e];
         for (int k = 1; k < rr; ++k) s += red[w][lane + k * units][e];
-        const int64_t o = i * v + (int64_t)lane * N + e;
-        y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+        if (ws != nullptr) {
+          ws[unit * v + (int64_t)lane * N + e] = s;  // the chunk's partial sum
+        } else {
+          const int64_t o = i * v + (int64_t)lane * N + e;
+          y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+        }
       }
     }
     __syncwarp();
@@ -1167,7 +1191,7 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // 5.8 TB/s; on aligned views it beats COLS only for short columns of
   // fp32/fp64 (n_k <= 128: +1-2 %; n_k = 2048 or bf16 lose)
   const bool long_ok = base_al && contiguous && v > kThreads / 2 && v <= kLongCols &&
-                       v * sb <= stb && nk < (1LL << 31) && u >= 16LL * sm_count() &&
+                       v * sb <= stb && nk * 8 <= 96 * 1024 && u >= 16LL * sm_count() &&
                        nk * v * sb + 16 > stb;
   const bool long_al_ok = long_ok && al_cols && nk <= 128 && sb >= 4 && v >= kThreads;
   // FLAT: aligned narrow contiguous slabs whose width's odd part is 1 or 3
@@ -1178,7 +1202,7 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   const int gg = vvu > 0 ? gcd_small(32, (int)std::min<int64_t>(vvu, 32)) : 1;
   const int64_t oddp = vvu / gg;
   const bool flat_ok = al_cols && contiguous && vvu >= 1 && vvu < 32 && (oddp == 1 || oddp == 3) &&
-                       gg >= 2 && nk * vvu >= 32 && nk < (1LL << 24);
+                       gg >= 2 && nk * vvu >= 32 && nk * 8 <= 96 * 1024;  // x lives in smem
   // FLAT_ROWS: short aligned contiguous rows of <= 32 vectors, odd part <= 7
   const int64_t nkv = nk / VEC;
   const int64_t rodd = nkv > 0 ? nkv / gcd_small(32, (int)std::min<int64_t>(nkv, 32)) : 0;
@@ -1195,7 +1219,7 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
                     (forced == REG_STAGED && stageable) || (forced == REG_FLAT && flat_ok) ||
                     (forced == REG_FLAT_ROWS && flat_rows_ok) ||
                     (forced == REG_STAGED_LONG && base_al && contiguous && v > 1 && v <= kLongCols &&
-                     v * sb <= stb && u > 1);
+                     v * sb <= stb && u > 1 && nk * 8 <= 96 * 1024);
     if (ok) return forced;
   }
   // measured on B200 (profiles/r01_regime_ab.txt): aligned views always stream
@@ -1204,6 +1228,12 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // SLABS.  Views whose rows/slabs are NOT 16-byte multiples and small enough
   // go through STAGED (contiguous cp.async tiles), which beats scalar loads
   // 2-4x there; larger unaligned views use the peeled / scalar forms.
+  // tall views -- few slabs, long columns -- are split-K SLABS: every other
+  // narrow or row regime gets about u warps, too few for 148 SMs (a single
+  // dot product would run on one warp)
+  if (u < 16LL * sm_count() && nk >= 8192 && v == 1) return REG_SLABS_U;
+  if (u < 16LL * sm_count() && nk >= 1024 && v > 1 && (al_cols ? v / VEC < 32 : v < 32))
+    return al_cols ? REG_SLABS : REG_SLABS_U;
   if (v == 1) {
     // rows of 3, 5, 6, 7 vectors idle 25-60 % of ROWS' power-of-two lane
     // groups; streamed flat they measured 6.2-6.35 vs 4.6-5.9 TB/s.  fp64
@@ -1296,6 +1326,66 @@ static void launch_rows_auto(const void* A, const void* x, void* y, int64_t u, i
   }
 }
 
+// ------------------------------------------------------------- SPLIT-K ----
+// Few, long outputs (u x column blocks too small to fill 148 SMs, n_k large:
+// tall-skinny views, single dot products, paper d = 2 k = 0): the rows are
+// cut into nch chunks, each chunk's partial sums go to a workspace in the
+// compute type, and k_split_fold adds the chunks of every output in chunk
+// order (deterministic) and applies the epilogue.
+template <int SD, typename C, bool WARP>
+__global__ void __launch_bounds__(256)
+    k_split_fold(const C* __restrict__ ws, int64_t nch, int64_t n, int64_t v,
+                 typename St<SD>::T* __restrict__ y, C alpha, C beta, int has_beta) {
+  if constexpr (WARP) {
+    // many chunks: a warp per output, lane l sums chunks l, l + 32, ... in
+    // order, then a fixed xor tree -- the same order on every call
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t o = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); o < n; o += warps) {
+      const int64_t i = o / v;
+      const C* p = ws + i * nch * v + (o - i * v);
+      C s = C(0);
+      for (int64_t ch = lane; ch < nch; ch += 32) s += p[ch * v];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+    }
+  } else {
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = o / v;
+      const C* p = ws + i * nch * v + (o - i * v);
+      C s = p[0];
+      for (int64_t ch = 1; ch < nch; ++ch) s += p[ch * v];
+      y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+    }
+  }
+}
+
+template <typename C>
+static C* split_alloc(int64_t elems, cudaStream_t st) {
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, (size_t)elems * sizeof(C), st) != cudaSuccess) {
+    cudaGetLastError();  // fall back to the unsplit launch
+    return nullptr;
+  }
+  return static_cast<C*>(p);
+}
+
+template <int SD, typename C>
+static void split_finish(C* ws, int64_t nch, int64_t u, int64_t v, void* y, C al, C be, int hb,
+                         cudaStream_t st) {
+  using T = typename St<SD>::T;
+  const int64_t n = u * v;
+  if (nch >= 32) {
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 8LL * sm_count()));
+    k_split_fold<SD, C, true><<<g, 256, 0, st>>>(ws, nch, n, v, (T*)y, al, be, hb);
+  } else {
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8LL * sm_count()));
+    k_split_fold<SD, C, false><<<g, 256, 0, st>>>(ws, nch, n, v, (T*)y, al, be, hb);
+  }
+  cudaFreeAsync(ws, st);
+}
+
 template <int SD, typename C>
 static void launch_staged(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t v,
                           C al, C be, int hb, cudaStream_t st) {
@@ -1386,24 +1476,43 @@ static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t
   const T* At = (const T*)A;
   const T* xt = (const T*)x;
   T* yt = (T*)y;
-  const unsigned b = (unsigned)blocks;
+  // split-K when the column blocks cannot fill the GPU (< 2 per SM; at 3.2
+  // per SM, paper d = 2 k = 0, splitting measured slower: 5.6 vs 5.9 TB/s)
+  int64_t nch = 1;
+  C* ws = nullptr;
+  if (blocks < 2LL * sm_count() && nk >= 512) {
+    nch = std::min<int64_t>(cdiv(8LL * sm_count(), blocks), nk / 128);
+    if (nch > 1 && (ws = split_alloc<C>(u * nch * v, st)) == nullptr) nch = 1;
+  }
+  const int64_t rpc = cdiv(nk, nch);
+  nch = cdiv(nk, rpc);
+  const dim3 b((unsigned)blocks, (unsigned)nch);
+  auto done = [&]() {
+    if (ws != nullptr) split_finish<SD, C>(ws, nch, u, v, y, al, be, hb, st);
+    return TV_OK;
+  };
   // unaligned, fp32/fp64: 3-row batches measured better for 4 row phases
   // (paper d = 3: 7.1-7.2 vs 6.6-6.8 TB/s) and for n_k <= 16 (d = 8: 6.4 vs
   // 6.1); 4 elsewhere (d = 2 k = 0 with 8 phases: 5.9 vs 5.1)
+  // the split-capable instantiation runs when splitting, and also for the
+  // unaligned single-phase form, where it compiles to 40 instead of 48
+  // registers and measured 3-6 % faster (paper d = 4..8, profiles/r01_cols_u_ab/)
+  const bool sp = nch > 1;
+  auto go = [&](auto kern) {
+    kern<<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb, rpc, ws);
+    return done();
+  };
   if (!AL && VEC <= 4 && (JR == 4 || (JR == 1 && nk <= 16))) {
     if (JR == 4)
-      k_cols<SD, C, 4, 3, false><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb);
-    else
-      k_cols<SD, C, 1, 3, false><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb);
-    return TV_OK;
+      return sp ? go(k_cols<SD, C, 4, 3, false, true>) : go(k_cols<SD, C, 4, 3, false, false>);
+    return go(k_cols<SD, C, 1, 3, false, true>);
   }
   switch (JR) {
-    case 1: k_cols<SD, C, 1, AL ? 8 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
-    case 2: k_cols<SD, C, 2, AL ? 8 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
-    case 4: k_cols<SD, C, 4, AL ? 4 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
-    default: k_cols<SD, C, 8, AL ? 4 : UA_UNR, AL><<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb); break;
+    case 1: return (sp || !AL) ? go(k_cols<SD, C, 1, AL ? 8 : UA_UNR, AL, true>) : go(k_cols<SD, C, 1, AL ? 8 : UA_UNR, AL, false>);
+    case 2: return sp ? go(k_cols<SD, C, 2, AL ? 8 : UA_UNR, AL, true>) : go(k_cols<SD, C, 2, AL ? 8 : UA_UNR, AL, false>);
+    case 4: return sp ? go(k_cols<SD, C, 4, AL ? 4 : UA_UNR, AL, true>) : go(k_cols<SD, C, 4, AL ? 4 : UA_UNR, AL, false>);
+    default: return sp ? go(k_cols<SD, C, 8, AL ? 4 : UA_UNR, AL, true>) : go(k_cols<SD, C, 8, AL ? 4 : UA_UNR, AL, false>);
   }
-  return TV_OK;
 }
 
 template <int SD, typename C>
@@ -1478,16 +1587,25 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       else go(k_flat<SD, C, 3, 2>);
       break;
     }
-    case REG_SLABS: {
-      const unsigned grid = grid_for(u, kWarps, 32);
-      k_slabs<SD, C, 4, true><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk,
-                                                         (int)v, su, sk, al, be, hb);
-      break;
-    }
+    case REG_SLABS:
     case REG_SLABS_U: {
-      const unsigned grid = grid_for(u, kWarps, 32);
-      k_slabs<SD, C, 8, false><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk,
-                                                          (int)v, su, sk, al, be, hb);
+      // split-K when there are too few slabs for the GPU's warps
+      int64_t nch = 1;
+      C* ws = nullptr;
+      if (u < 32LL * sm_count() && nk >= 256) {
+        nch = std::min<int64_t>(cdiv(32LL * sm_count(), u), nk / 64);
+        if (nch > 1 && (ws = split_alloc<C>(u * nch * v, st)) == nullptr) nch = 1;
+      }
+      const int64_t rpc = cdiv(nk, nch);
+      nch = cdiv(nk, rpc);
+      const unsigned grid = grid_for(u * nch, kWarps, 32);
+      if (reg == REG_SLABS)
+        k_slabs<SD, C, 4, true><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
+                                                           su, sk, al, be, hb, nch, rpc, ws);
+      else
+        k_slabs<SD, C, 8, false><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
+                                                            su, sk, al, be, hb, nch, rpc, ws);
+      if (ws != nullptr) split_finish<SD, C>(ws, nch, u, v, y, al, be, hb, st);
       break;
     }
     default: {

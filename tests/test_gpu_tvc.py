@@ -310,3 +310,26 @@ def test_large_views_sampled_exact(tv, mode_name, shape):
             vals = (O.fill_hash(9, g.astype(np.uint64)) % np.uint64(97)).astype(np.float64) + 1.0
             want = O.demote(np.array([np.dot(vals, O.promote(xs, mode_name).astype(np.float64))]), mode_name)
             assert np.array_equal(_bits(y[i * v + l: i * v + l + 1]), _bits(want)), (k, i, l)
+
+
+TALL = [((300_000, 8), 0, "slabs"), ((1, 200_000, 16), 1, "slabs"), ((100_000, 160), 0, "cols"),
+        ((40_001, 301), 0, "cols_u"), ((1, 3_000_000), 1, "slabs_u"), ((3, 100_001, 7), 1, "slabs_u"),
+        ((2, 50_000, 24), 1, "slabs"), ((70_000, 2), 0, "slabs_u")]
+
+
+@pytest.mark.parametrize("mode_name", ["f64", "f32", "bf16f32", "f16f32"])
+@pytest.mark.parametrize("shape,k,regime", TALL)
+def test_tall_views_split_k_bitwise(tv, mode_name, shape, k, regime):
+    """Few slabs, long columns: the rows are split into chunks whose partial
+    sums are folded in chunk order (split-K) -- integer data, so bitwise."""
+    mode = tv.MODES[mode_name]
+    rng = np.random.default_rng(hash((shape, k)) % 2**32)
+    vals = rng.integers(1, 4, shape).astype(np.float64)
+    x64 = rng.integers(1, 3, shape[k]).astype(np.float64)
+    t = tv.Tensor.from_array(vals, mode)
+    xs = O.demote(x64, mode_name).copy()
+    if mode_name == "f32":
+        assert tv.tvc_regime(t, k) == regime
+    y = tv.tvc_native(t, xs, k, alpha=2.0)
+    want = O.tvc(O.demote(vals.reshape(-1), mode_name), shape, xs, k, mode_name, alpha=2.0)
+    assert np.array_equal(_bits(y.to_numpy()), _bits(want)), (shape, k, mode_name, tv.tvc_regime(t, k))
