@@ -70,12 +70,14 @@ def _peaks() -> dict:
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
-def _traffic(workload: str, kernel: str):
-    """dram bytes per launch from the committed ncu capture, if any."""
+def _traffic(workload: str, kernel: str, world: int = 1):
+    """dram bytes per launch from the committed ncu capture of this exact
+    launch (workload at this GPU count), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             data = json.load(fh)
-        return data.get(workload, {}).get(kernel)
+        key = workload if world == 1 else f"{workload}_n{world}"
+        return data.get(key, {}).get(kernel)
     except (OSError, ValueError):
         return None
 
@@ -369,7 +371,7 @@ def run_ours(args) -> dict | None:
         "roofline_frac_aggregate": round(value / (peak * world), 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4),
-                     "traffic": _traffic(args.workload, f"k{kd}"),
+                     "traffic": None if args.shape else _traffic(args.workload, f"k{kd}", world),
                      "kernel": f"tv_tvc k={kd} ({regimes[kd]})",
                      "bytes_per_launch": mode_bytes[kd],
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
