@@ -533,6 +533,7 @@ def run_e2e_sweep(args, tv, dt, part, xs, s, world, rank, group, job_bytes_step)
 
 
 def run_hopm(args, tv, dt, world, rank, wl, mode, group):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -561,6 +562,32 @@ def run_hopm(args, tv, dt, world, rank, wl, mode, group):
     job = sum(per_rank)
     value = job * sweeps / (ms / 1e3) / 1e9
     peak = float(_peaks().get("hbm_gbs", 6650.0))
+
+    # roofline: the two full-slab contractions that carry ~99 % of a sweep's
+    # bytes (the first TVC of iterations j = 0 and j = 1), each timed alone on
+    # this rank's slab after the timed region (blocking kernel ahead)
+    part = next(p for p in dt.parts if p is not None)
+    d = part.order
+    kern = []
+    for j in (0, 1):
+        k = tv.iteration_plan(d, j, True)[1][0]
+        n_k = part.shape.extents[k]
+        xk = tv.demote(np.ones(n_k), mode)
+        outk = torch.empty(part.size // n_k, dtype=mode.torch_storage, device="cuda")
+        tv.tvc_native(part, xk, k, out=outk)
+        _block_stream(torch)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record()
+        for _ in range(3):
+            tv.tvc_native(part, xk, k, out=outk)
+        k1.record()
+        torch.cuda.synchronize()
+        kms = k0.elapsed_time(k1) / 3
+        nbytes = (part.size + n_k + part.size // n_k) * mode.storage_bytes
+        kern.append({"k": k, "regime": tv.tvc_regime(part, k), "ms": round(kms, 4),
+                     "gbs": round(nbytes / kms / 1e6, 1), "bytes": nbytes})
+        del outk
+    dom = max(kern, key=lambda e: e["ms"])
     if rank != 0:
         return None
     return {
@@ -573,6 +600,12 @@ def run_hopm(args, tv, dt, world, rank, wl, mode, group):
                    "split_mode": wl["s"], "p": world, "parallelism": f"split{world}"},
         "per_gpu_gbs": round(value / world, 2),
         "roofline_frac_aggregate": round(value / (peak * world), 4),
+        "roofline": {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": round(dom["gbs"] / peak, 4), "traffic": None,
+                     "kernel": f"tv_tvc k={dom['k']} ({dom['regime']}) on the rank's full slab",
+                     "bytes_per_launch": dom["bytes"]},
+        "full_slab_passes": kern,
+        "tvc_launches": res.tvc_count,
         "lambda_last": res.norms[-1][-1],
         "clocks": clk,
     }
