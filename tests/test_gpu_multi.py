@@ -43,7 +43,7 @@ def _worker(rank, world, port, q):
         # dtvc on a device-generated 5-mode tensor: every k, split on / off k
         shape = (6, 8, world * 3, 5, 4)
         full = O.fill_values(shape, "hash", seed=4).reshape(shape)
-        for name in ("f64", "f32", "bf16f32", "f16f32"):
+        for name in ("f64", "f32", "f32f64", "bf16f32", "f16f32"):
             mode = tv.MODES[name]
             host = O.demote(full.reshape(-1), name).reshape(shape)
             for s in sorted({2} | ({4} if tv.make_split_plan(4, 4, world).p_eff == world else set())):
@@ -86,7 +86,7 @@ def _worker(rank, world, port, q):
         for fshape, s in (((5, 6, world * 3, 7), 2), ((world * 4, 30, 7), 0), ((3, world * 2, 50), 1),
                           ((2, world * 3, 40), 1)):
             fullf = O.fill_values(fshape, "hash", seed=8).reshape(fshape)
-            for name in ("f64", "f32", "bf16f32", "f16f32"):
+            for name in ("f64", "f32", "f32f64", "bf16f32", "f16f32"):
                 mode = tv.MODES[name]
                 hostf = O.demote(fullf.reshape(-1), name).reshape(fshape)
                 x = O.demote((np.arange(fshape[s]) % 7) + 1.0, name).copy()
@@ -120,7 +120,7 @@ def _worker(rank, world, port, q):
                        bool(np.allclose(O.promote(got, name), O.promote(want, name), rtol=1e-2 if name == "bf16f32" else 1e-6))))
         # the dHOPM3 reduction with the normalisation in the fold's epilogue:
         # the same bits as all_reduce_sum + normalize
-        for name in ("f64", "f32", "bf16f32", "f16f32"):
+        for name in ("f64", "f32", "f32f64", "bf16f32", "f16f32"):
             mode = tv.MODES[name]
             for n in (384, 4096, 1001):
                 v = torch.from_numpy(O.demote(np.random.default_rng(rank + n).standard_normal(n), name).copy())
