@@ -49,11 +49,6 @@ def main() -> int:
             _lib.check(lib.tv_getvc(1, part.buf.data_ptr() + lo * sb, 0, 0, nk, hi - lo, v, xv.data_ptr(), 1.0,
                                     0.0, ptrs[c] + rank * slot_bytes, _lib.stream_ptr()))
 
-    def scatter1():
-        dsts = (ctypes.c_void_p * p)(*[ptrs[c] + rank * slot_bytes for c in range(p)])
-        _lib.check(lib.tv_tvc_scatter(part.buf.data_ptr(), 0, 0, 1, nk, v, xv.data_ptr(), dsts, p, chunk,
-                                      _lib.stream_ptr()))
-
     def barrier():
         hdl.barrier(channel=0)
 
@@ -85,7 +80,7 @@ def main() -> int:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return round(float(t.item()), 1)
 
-    res = {"local_tvc_us": timed(local), "scatter_us": timed(scatter), "scatter1_us": timed(scatter1), "barrier_us": timed(barrier),
+    res = {"local_tvc_us": timed(local), "scatter_us": timed(scatter), "barrier_us": timed(barrier),
            "fold_us": timed(fold), "gather_us": timed(gather), "full_us": timed(full)}
     if rank == 0:
         print(json.dumps({"world": p, **res}), flush=True)
