@@ -333,3 +333,27 @@ def test_tall_views_split_k_bitwise(tv, mode_name, shape, k, regime):
     y = tv.tvc_native(t, xs, k, alpha=2.0)
     want = O.tvc(O.demote(vals.reshape(-1), mode_name), shape, xs, k, mode_name, alpha=2.0)
     assert np.array_equal(_bits(y.to_numpy()), _bits(want)), (shape, k, mode_name, tv.tvc_regime(t, k))
+
+
+def test_getvc_tall_strided_views_split_k(tv):
+    """Strided tall views through getvc take the split-K forms: a vecmat over
+    a 200 000 x 8 column window (lda 12), a matvec that is one 3 M-element dot
+    product, and a wide-but-short-grid vecmat (lda > n); integer data, so the
+    chunked sums are exact."""
+    g = torch.Generator(device="cpu").manual_seed(5)
+    big = torch.randint(1, 4, (200_000, 12), generator=g).to(torch.float64).cuda()
+    view = big[:, 2:10]
+    xv = torch.randint(1, 3, (200_000,), generator=g).to(torch.float64).cuda()
+    yv = torch.empty(8, dtype=torch.float64, device="cuda")
+    tv.getvc(tv.VECMAT, 1.0, view, xv, 0.0, yv)
+    assert torch.equal(yv, xv @ view)
+    row = torch.randint(1, 4, (1, 3_000_000), generator=g).to(torch.float64).cuda()
+    xr = torch.randint(1, 3, (3_000_000,), generator=g).to(torch.float64).cuda()
+    yr = torch.empty(1, dtype=torch.float64, device="cuda")
+    tv.getvc(tv.MATVEC, 2.0, row, xr, 0.0, yr)
+    assert torch.equal(yr, 2.0 * (row @ xr))
+    wide = torch.randint(1, 4, (50_000, 300), generator=g).to(torch.float64).cuda()[:, :257]
+    xw = torch.randint(1, 3, (50_000,), generator=g).to(torch.float64).cuda()
+    yw = torch.full((257,), 3.0, dtype=torch.float64, device="cuda")
+    tv.getvc(tv.VECMAT, 1.0, wide, xw, 0.5, yw)
+    assert torch.equal(yw, xw @ wide + 1.5)
