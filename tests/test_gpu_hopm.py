@@ -395,3 +395,23 @@ def test_dtvc_sweep_on_result_reports_every_mode(tv):
     assert sorted(k for k, _ in seen) == [0, 1, 2]
     for k, r in seen:
         assert r is res[k]
+
+
+def test_dhopm3_graph_replay_equals_eager(tv):
+    """graph=True: sweeps after the first replay one captured CUDA graph --
+    bitwise the eager run's vectors and norms, identical counters."""
+    rng = np.random.default_rng(21)
+    for shape, name in (((12, 11, 10), "f64"), ((9, 8, 7, 6), "f64"), ((16, 12, 20), "bf16f32"),
+                        ((40, 30), "f32"), ((600, 500, 3), "f64")):
+        mode = tv.MODES[name]
+        A = tv.Tensor.from_array(rng.standard_normal(shape), mode)
+        x0 = tv.initial_vectors(A.shape, mode)
+        eager = tv.dhopm3(tv.distribute(A, 0, 1), [v.copy() for v in x0], sweeps=4)
+        graph = tv.dhopm3(tv.distribute(A, 0, 1), [v.copy() for v in x0], sweeps=4, graph=True)
+        for a, b in zip(eager.vectors, graph.vectors):
+            assert np.array_equal(_bits(a), _bits(b)), (shape, name)
+        assert eager.norms == graph.norms, (shape, name)
+        assert eager.iteration_touched == graph.iteration_touched
+        assert eager.tvc_count == graph.tvc_count
+        assert eager.kernel_counters[0] == graph.kernel_counters[0]
+        assert eager.comm_counters[0] == graph.comm_counters[0]
