@@ -21,6 +21,15 @@
 //   SLABS       1 < v < 32 units: one warp per slab, R = 32 / units rows per
 //               step so each warp load is one contiguous run, then a
 //               fixed-order fold across rows in shared memory.
+//   FLAT /      narrow aligned slabs / short aligned rows streamed as flat
+//   FLAT_ROWS   warp runs of 16-byte vectors, lanes mapped to columns by gcd.
+//   STAGED      slabs that fit a 48 KB tile (odd extents, short rows): whole-
+//               slab tiles moved by ONE TMA bulk copy each (cp.async.bulk on
+//               mbarriers, double-buffered), dot products from shared memory.
+//   STAGED_LONG larger slabs of <= 4096 columns: row-run tiles, one bulk copy
+//               each, column sums kept in registers across a slab's tiles.
+//   split-K     few outputs, long columns (COLS / SLABS): row chunks write
+//               partial sums to a workspace folded in chunk order.
 //
 // Every regime has an aligned form (one 16-byte ld.global.nc.L1::no_allocate
 // per lane, "unit" = 16 bytes) and an unaligned form for rows or slabs that do
