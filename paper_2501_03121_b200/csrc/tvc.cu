@@ -1159,7 +1159,16 @@ static int pick_row_group(int64_t nunits) {
 // row phases of the COLS kernel: enough rows per warp for deep load
 // pipelines, as many 32-lane stripes per CTA as the slab is wide, and at
 // least 4 CTAs per SM so small views still fill the GPU
-static int pick_col_phases(int64_t nk, int64_t stripes, int64_t u) {
+static int pick_col_phases(int64_t nk, int64_t stripes, int64_t u, int sb = 0) {
+  static const int jr_env = [] {  // TENVEC_B200_COL_JR: row phases, for A/B runs
+    const char* e = getenv("TENVEC_B200_COL_JR");
+    return e ? atoi(e) : 0;
+  }();
+  if (jr_env == 1 || jr_env == 2 || jr_env == 4 || jr_env == 8) return jr_env;
+  // one fp64 slab with plenty of stripes (C2 k = 0, C4 k = 0): whole columns
+  // per warp measured faster than row phases (7.35 vs 7.24 TB/s, 7.20 vs
+  // 7.10; profiles/r01_cols_jr_ab/) -- not for narrower types or few stripes
+  if (sb == 8 && u == 1 && cdiv(stripes, kWarps) >= 16LL * sm_count()) return 1;
   int jr = nk >= 1024 ? 8 : nk >= 512 ? 4 : nk >= 256 ? 2 : 1;
   int cw_max = 1;
   while (cw_max < kWarps && cw_max * 2 <= stripes) cw_max *= 2;
@@ -1478,7 +1487,7 @@ static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t
   constexpr int VEC = VecN<SD>::N;
   constexpr int UA_UNR = VEC >= 8 ? 2 : 4;  // scalar loads in flight: UNR * VEC (8 measured slower)
   const int64_t stripes = cdiv(v, 32 * VEC);
-  const int JR = pick_col_phases(nk, stripes, u);
+  const int JR = pick_col_phases(nk, stripes, u, AL ? (int)sizeof(T) : 0);
   const int64_t ntile = cdiv(stripes, kWarps / JR);
   const int64_t blocks = u * ntile;
   if (blocks > 0x7fffffffLL) return set_error(TV_EKERNEL, "tv_tvc: view too large for COLS grid");
