@@ -1290,6 +1290,11 @@ int regime_of(const void* A, int storage, int64_t u, int64_t nk, int64_t v) {
 }
 
 constexpr int kRowBatch = 4;  // 16-byte loads per lane per batch
+// long aligned rows (batched loop, register double buffer): 6 loads per
+// lane per batch measured 1.5 % faster than 4 on C2 k = 2 (7.42 vs 7.31
+// TB/s, profiles/r01_rows_ab/rq*; 8 no better); peeled rows keep 4 (paper
+// d = 3 k = 2: 6.6 vs 6.9)
+constexpr int kRowBatchLong = 6;
 
 template <int SD, typename C, int G, int RS, bool PEEL, bool LONG>
 static void launch_rows(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t su,
@@ -1299,7 +1304,7 @@ static void launch_rows(const void* A, const void* x, void* y, int64_t u, int64_
   const int64_t rows_per_block = (int64_t)kWarps * (32 / G) * RS;
   const unsigned grid = grid_for(u, rows_per_block, 32);
   if (xs_bytes <= 96 * 1024) {
-    auto kern = k_rows<SD, C, G, RS, kRowBatch, true, PEEL, LONG>;
+    auto kern = k_rows<SD, C, G, RS, (LONG && !PEEL) ? kRowBatchLong : kRowBatch, true, PEEL, LONG>;
     if (xs_bytes > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs_bytes);
     kern<<<grid, kThreads, xs_bytes, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
