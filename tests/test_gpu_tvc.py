@@ -291,7 +291,9 @@ def test_c1_256_cubed_every_mode_bitwise(tv):
                                              ("bf16f32", (2048, 2048, 256)),
                                              # past 2**32 elements (int64 indexing), and odd
                                              # extents past 2**31 (unaligned regimes)
-                                             ("f32", (2048, 2048, 1040)), ("f64", (1501, 1499, 1001))])
+                                             ("f32", (2048, 2048, 1040)), ("f64", (1501, 1499, 1001)),
+                                             # one fp64 slab with many stripes: whole-column COLS
+                                             ("f64", (64, 1_310_720))])
 def test_large_views_sampled_exact(tv, mode_name, shape):
     """Full-size-style views checked on sampled outputs regenerated from the
     closed-form hash fill (size-independent, exact for integer data)."""
