@@ -27,6 +27,7 @@ Counters follow the reference's ring accounting (comm.py:64-81).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import time
 import warnings
@@ -404,7 +405,8 @@ class RankGroup:
 
     def _owner_streams(self, device) -> tuple:
         if getattr(self, "_lanes", None) is None:
-            self._lanes = (torch.cuda.Stream(device=device), torch.cuda.Stream(device=device))
+            n = int(os.environ.get("TENVEC_B200_OWNER_LANES", "2"))
+            self._lanes = tuple(torch.cuda.Stream(device=device) for _ in range(max(1, n)))
         return self._lanes
 
     def tvc_reduce_fused(self, part, xv: torch.Tensor, k: int, mode: PrecisionMode,
@@ -461,15 +463,15 @@ class RankGroup:
         lanes = self._owner_streams(part.buf.device)
         for ls in lanes:
             ls.wait_stream(main)
-        xv.record_stream(lanes[0])
-        xv.record_stream(lanes[1])
+        for ls in lanes:
+            xv.record_stream(ls)
         for j in range(p):  # own range first, then the peers in ring order
             c = (rank + j) % p
             lo, hi = bounds[c]
             if hi <= lo:
                 continue
             dst = ptrs[c] + rank * slot_bytes
-            ls = _lib.stream_ptr(lanes[j % 2])
+            ls = _lib.stream_ptr(lanes[j % len(lanes)])
             if along_u:
                 rc = lib.tv_tvc(a_ptr + lo * nk * v * sb, st_, ct_, hi - lo, nk, v, xv.data_ptr(),
                                 1.0, 0.0, dst, ls)
