@@ -4,15 +4,20 @@
  *
  * Every entry point takes plain device pointers owned by the caller, element
  * counts, and a cudaStream_t passed as void*.  All work is enqueued
- * asynchronously on that stream; nothing here allocates device memory or
- * synchronises the host.  Return value: TV_OK (0) or an error code; the
- * thread-local tv_last_error() gives the message.  There is no CPU fallback:
- * a missing or failing device raises TV_ECUDA.
+ * asynchronously on that stream; nothing synchronises the host.  Device
+ * memory: the only allocation is the split-K workspace of tv_tvc / tv_getvc
+ * on views with few, long outputs (stream-ordered cudaMallocAsync, freed on
+ * the same stream; failure returns TV_ECUDA, never a different kernel).
+ * tv_tvc_ws / tv_getvc_ws take that workspace from the caller instead (size
+ * from tv_tvc_workspace_bytes / tv_getvc_workspace_bytes) and allocate
+ * nothing -- the Python package always uses them.  Return value: TV_OK (0)
+ * or an error code; the thread-local tv_last_error() gives the message.
+ * There is no CPU fallback: a missing or failing device raises TV_ECUDA.
  *
  * Reference interfaces replaced (paths relative to the reference pkg/src/tenvec):
- *   tv_tvc          kernels.py:126-171  tvc_native (and getvc, kernels.py:73-123,
+ *   tv_tvc, tv_tvc_ws kernels.py:126-171 tvc_native (and getvc, kernels.py:73-123,
  *                                       through the (u, n_k, v) block view)
- *   tv_getvc        kernels.py:73-123   getvc over a strided m x n view (lda >= n)
+ *   tv_getvc(_ws)   kernels.py:73-123   getvc over a strided m x n view (lda >= n)
  *   tv_convert      precision.py:109-128 promote / demote (bit-exact semantics)
  *   tv_norm2        kernels.py:234-239  norm2
  *   tv_normalize    kernels.py:242-254  normalize
@@ -21,6 +26,8 @@
  *   tv_rank_fold    comm.py:84-100      ring_all_reduce (ascending-rank fold) and
  *                   comm.py:103-134     ring_all_reduce_mixed (chunk c starts at rank c,
  *                                       demote(promote+promote) per hop)
+ *   tv_peer_barrier comm.py:202-235     the WorkerGroup rendezvous slot + timeout, as a
+ *                                       stream-ordered barrier over peer memory
  *   tv_fill         bench.py:62-80      fill_array (ones / ramp; "hash" replaces numpy's
  *                                       integer-random with a counter hash in [1, 97])
  */
@@ -73,6 +80,20 @@ const char* tv_last_error(void);
 int tv_tvc(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
            const void* x, double alpha, double beta, void* y, void* stream);
 
+/* Bytes of split-K workspace tv_tvc needs for this view (0 when the view
+ * does not split; -1 on invalid arguments).  A pure function of (A's
+ * alignment, storage, compute, u, nk, v) and the device's SM count: a view
+ * always splits the same way, so its summation order never depends on
+ * memory availability. */
+int64_t tv_tvc_workspace_bytes(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v);
+
+/* tv_tvc with a caller-provided split-K workspace (16-byte aligned, at least
+ * tv_tvc_workspace_bytes; may be NULL when that is 0).  Allocates nothing:
+ * safe inside CUDA graph capture; TV_EKERNEL if the workspace is short. */
+int tv_tvc_ws(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
+              const void* x, double alpha, double beta, void* y, void* ws, int64_t ws_bytes,
+              void* stream);
+
 /* The same contraction through the naive scalar kernel only (one thread per
  * output for v > 1, one warp per row for v == 1): the "looped" cross-check of
  * tv_tvc's regime kernels, used by tvc_looped_oracle (kernels.py:174-188). */
@@ -111,6 +132,14 @@ int tv_set_regime_override(int regime);
  * trans 0 = matvec (x has n, y has m), 1 = vecmat (x has m, y has n). */
 int tv_getvc(int trans, const void* A, int storage, int compute, int64_t m, int64_t n,
              int64_t lda, const void* x, double alpha, double beta, void* y, void* stream);
+
+/* Split-K workspace of tv_getvc for this view, and tv_getvc with it supplied
+ * by the caller (as tv_tvc_workspace_bytes / tv_tvc_ws). */
+int64_t tv_getvc_workspace_bytes(int trans, const void* A, int storage, int compute, int64_t m, int64_t n,
+                                 int64_t lda);
+int tv_getvc_ws(int trans, const void* A, int storage, int compute, int64_t m, int64_t n, int64_t lda,
+                const void* x, double alpha, double beta, void* y, void* ws, int64_t ws_bytes,
+                void* stream);
 
 /* dst[i] = convert(src[i]) with reference semantics: widening is exact,
  * f64->f32 and ->f16 round to nearest even (f16 overflow -> inf), ->bf16
@@ -171,6 +200,24 @@ int tv_rank_fold_range(const void* src, int64_t src_stride_elems, int p, int64_t
  * peer-memory allreduce, where rank r's buffer holds reduced ring chunk r. */
 int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t chunk, int dtype,
                    void* dst, void* stream);
+
+/* Bytes at the start of a peer buffer reserved for the barrier words
+ * (uint32 per rank); the transports put their data after it. */
+#define TV_PEER_HEADER 4096
+
+/* Stream-ordered barrier of p ranks over peer memory (the device form of the
+ * WorkerGroup rendezvous, comm.py:202-235).  peer_bases is a HOST array of
+ * the p ranks' peer-buffer bases as mapped in this process (zeroed headers
+ * before the first barrier); epoch counts this group's barriers from 1 and
+ * must be the same on every rank.  One single-CTA kernel: posts epoch into
+ * word [rank] of every peer's header (release, system scope), then waits for
+ * word [j] of its own header to reach epoch for every j (acquire).  Past
+ * timeout_ns (<= 0: wait forever) it does NOT trap: it writes status[0] =
+ * TV_ECOLL, status[1] = epoch, status[2..3] = bit mask of the ranks still
+ * missing (device int32[4], zero on entry) and returns; while status[0] is
+ * set, later barriers post their arrival without waiting. */
+int tv_peer_barrier(void* const* peer_bases, int p, int rank, uint32_t epoch, int64_t timeout_ns,
+                    int32_t* status, void* stream);
 
 /* Fill the rank-local slab [s_lo, s_hi) along mode s of a global tensor with
  * extents ext[0..d-1] (last mode fastest) from the GLOBAL linear index g:

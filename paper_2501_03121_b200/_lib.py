@@ -23,6 +23,7 @@ LIB_PATH = Path(_os.environ.get("TENVEC_B200_LIB") or
 TV_F64, TV_F32, TV_F16, TV_BF16 = 0, 1, 2, 3
 TV_FILL_ONES, TV_FILL_RAMP, TV_FILL_HASH = 0, 1, 2
 TV_MAX_RANKS = 64
+TV_PEER_HEADER = 4096
 REGIMES = {0: "naive", 1: "rows", 2: "rows_short", 3: "cols", 4: "slabs", 5: "rows_u", 6: "cols_u",
            7: "slabs_u", 8: "staged", 9: "flat",
            10: "flat_rows", 11: "staged_long"}
@@ -36,6 +37,12 @@ SIGNATURES = {
     "tv_version": (ctypes.c_char_p, []),
     "tv_last_error": (ctypes.c_char_p, []),
     "tv_tvc": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),
+    "tv_tvc_ws": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp,
+                          _i64, _vp]),
+    "tv_tvc_workspace_bytes": (_i64, [_vp, _int, _int, _i64, _i64, _i64]),
+    "tv_getvc_ws": (_int, [_int, _vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double,
+                           _vp, _vp, _i64, _vp]),
+    "tv_getvc_workspace_bytes": (_i64, [_int, _vp, _int, _int, _i64, _i64, _i64]),
     "tv_tvc_naive": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),
     "tv_tvc_normalize": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tv_tvc_regime": (_int, [_vp, _int, _i64, _i64, _i64]),
@@ -50,6 +57,7 @@ SIGNATURES = {
                                        _vp]),
     "tv_rank_fold_range": (_int, [_vp, _i64, _int, _i64, _i64, _i64, _int, _int, _int, _vp, _vp]),
     "tv_rank_select": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp]),
+    "tv_peer_barrier": (_int, [ctypes.POINTER(_vp), _int, _int, ctypes.c_uint32, _i64, _vp, _vp]),
     "tv_fill": (_int, [_vp, _int, _int, ctypes.c_uint64, ctypes.POINTER(_i64), _int, _int, _i64, _i64, _vp]),
     "tv_axpby": (_int, [ctypes.c_double, _vp, ctypes.c_double, _vp, _int, _int, _i64, _vp]),
     "tv_read_stream": (_int, [_vp, _i64, _vp, _vp]),

@@ -26,6 +26,8 @@ Counters follow the reference's ring accounting (comm.py:64-81).
 
 from __future__ import annotations
 
+import collections
+import contextlib
 import ctypes
 import os
 import threading
@@ -40,10 +42,12 @@ from . import _lib
 from .errors import CollectiveError, CollectiveTimeout
 from .precision import PrecisionMode, tv_dtype_of
 from .tensor import as_bits
+from .transport import PeerBuffer, PeerMemoryUnavailable, TorchTransport
 
 __all__ = [
     "CollectiveError", "CollectiveTimeout", "CommCounters", "ring_chunks", "ring_all_reduce",
     "ring_all_reduce_mixed", "ring_all_gather", "WorkerGroup", "RankGroup", "device_fold",
+    "FusedPlan", "fused_plan", "PeerMemoryUnavailable",
 ]
 
 
@@ -65,6 +69,10 @@ def ring_chunks(n: int, p: int) -> list[tuple[int, int]]:
     """ceil(n/p)-sized chunks with a short (possibly empty) tail (comm.py:58-61)."""
     q = -(-n // p) if n else 0
     return [(min(i * q, n), min((i + 1) * q, n)) for i in range(p)]
+
+
+def ring_sizes(n: int, p: int):
+    return (b - a for a, b in ring_chunks(n, p))
 
 
 def _charge(counters, sender: int, receiver: int, size: int) -> None:
@@ -312,6 +320,7 @@ class WorkerGroup:
 
 
 FoldFn = Callable[..., None]
+ALGOS = ("exact", "nccl", "p2p", "fused")
 
 
 def _wire(t: torch.Tensor) -> torch.Tensor:
@@ -319,234 +328,419 @@ def _wire(t: torch.Tensor) -> torch.Tensor:
     return t.view(torch.bfloat16) if t.dtype == torch.uint16 else t
 
 
-class RankGroup:
-    """This process is rank ``rank`` of ``size`` (torch.distributed).  Same
-    method names as ``WorkerGroup`` so the dtvc / dhopm3 rank bodies run
-    unchanged; the rank argument must be this process's rank.
+def _env_int(name: str, default: int, lo: int) -> int:
+    raw = os.environ.get(name, "").strip()
+    if not raw:
+        return default
+    try:
+        val = int(raw)
+    except ValueError:
+        raise CollectiveError(f"{name}={raw!r} is not an integer") from None
+    if val < lo:
+        raise CollectiveError(f"{name}={val} must be >= {lo}")
+    return val
 
-    ``fold`` is the local reduction (default: the tv_rank_fold kernel); CPU
-    multi-process tests inject a host fold to exercise the chunk logic over
-    gloo without a GPU.
+
+@dataclass(frozen=True)
+class FusedPlan:
+    """Index math of the split-mode contraction fused with its reduction
+    (RankGroup.tvc_reduce_fused) for a rank-local (u, n_k, v) view over p
+    ranks.  The (u, v) output is cut into p owner ranges along u (whole slabs,
+    u >= p) or along v (columns, u == 1); owner c receives every rank's
+    partial sums of its range in p slots of ``slot_elems`` and keeps the
+    folded range in slot p."""
+
+    along_u: bool
+    outer: int            # extent that is partitioned (u or v)
+    q: int                # outer indices per owner (the last owner may hold fewer)
+    unit: int             # output elements per outer index
+    bounds: tuple         # per owner: [lo, hi) outer indices
+    sizes: tuple          # per owner: output elements
+    chunk: int            # output elements of a full owner range
+    ring_chunk: int       # ring_chunks' chunk of the whole output (mixed fold order)
+    slot_elems: int
+    slot_bytes: int
+
+    @property
+    def n(self) -> int:
+        return sum(self.sizes)
+
+
+def fused_plan(u: int, v: int, p: int, storage_bytes: int) -> FusedPlan | None:
+    """None when the view has no owner partition (p == 1, or 1 < u < p)."""
+    if p == 1 or not (u >= p or u == 1):
+        return None
+    along_u = u >= p
+    outer = u if along_u else v
+    q = -(-outer // p)
+    unit = v if along_u else 1
+    bounds = tuple((min(c * q, outer), min((c + 1) * q, outer)) for c in range(p))
+    sizes = tuple((b - a) * unit for a, b in bounds)
+    chunk = q * unit
+    ring = ring_chunks(u * v, p)
+    slot_bytes = -(-chunk * storage_bytes // 16) * 16
+    return FusedPlan(along_u, outer, q, unit, bounds, sizes, chunk, ring[0][1] - ring[0][0],
+                     slot_bytes // storage_bytes, slot_bytes)
+
+
+class RankGroup:
+    """This process is rank ``rank`` of ``size``.  Same method names as
+    ``WorkerGroup`` so the dtvc / dhopm3 rank bodies run unchanged; the rank
+    argument must be this process's rank.
+
+    ``transport`` moves the bytes (default ``TorchTransport``: torch.distributed
+    over NCCL/NVLink plus symmetric memory; ``loopback.LoopbackTransport`` runs
+    the same code as thread-ranks on one GPU).  ``fold`` is the local reduction
+    (default: the tv_rank_fold kernel); CPU multi-process tests inject a host
+    fold to exercise the chunk logic over gloo without a GPU.
 
     ``algo`` (default from TENVEC_B200_ALLREDUCE, else "fused"):
       exact  all-to-all of ring chunks + fold kernel + all-gather (NCCL moves
              the bytes), reference-exact;
-      p2p    the same fold over PEER memory: every rank's buffer is a
-             symmetric-memory allocation (torch symm_mem, NVLink mapped), rank c
-             folds ring chunk c straight from its peers' buffers with the fold
-             kernel, a select kernel gathers the reduced chunks; three device
-             barriers, no NCCL, reference-exact;
+      p2p    the same fold over PEER memory: every rank's buffer is mapped
+             into its peers (NVLink), rank c folds ring chunk c straight from
+             its peers' buffers with the fold kernel, a select kernel gathers
+             the reduced chunks; three device barriers, no NCCL, reference-exact;
       nccl   ncclAllReduce (rank-consistent, not reference-ordered);
       fused  for dtvc's split-mode contraction (k == s): the TVC itself writes
              each owner's output range straight into that owner's receive slot
-             in peer (symmetric) memory over NVLink, the owner folds its p
-             slots in the reference order, and every rank gathers the reduced
-             ranges from its peers (``tvc_reduce_fused``); no NCCL, no partial
-             written to local HBM first.  Other reductions run as "exact";
-             without symmetric memory the group falls back to "exact".
+             in peer memory, the owner folds its p slots in the reference
+             order, and every rank gathers the reduced ranges from its peers
+             (``tvc_reduce_fused``); no NCCL, no partial written to local HBM
+             first.  Other reductions run as "exact"; when any rank cannot map
+             peer memory, every rank falls back to "exact" together.
+
+    Failure semantics (comm.py:206-235, 279-284): collectives are numbered in
+    issue order; ``timeout`` (default TENVEC_B200_TIMEOUT, else 300 s) bounds
+    every device barrier (tv_peer_barrier records the missing ranks instead of
+    hanging), every host collective and ``wait()``.  A timeout raises
+    ``CollectiveTimeout(kind, absent)``, the absent ranks read from the device
+    barrier's status or from a ledger of issued collectives in the store, and
+    leaves the group failed.  ``check=True`` (or
+    TENVEC_B200_CHECK_COLLECTIVES=1) also meets every rank in the store before
+    each collective, raising CollectiveError on a kind mismatch the way the
+    reference's rendezvous slot does (one store round trip per collective).
     """
 
-    def __init__(self, group=None, *, algo: str | None = None, fold: FoldFn | None = None):
-        import os
-
-        import torch.distributed as dist
-
-        if not dist.is_initialized():
-            raise CollectiveError("torch.distributed is not initialised")
+    def __init__(self, group=None, *, algo: str | None = None, fold: FoldFn | None = None,
+                 timeout: float | None = None, transport=None, check: bool | None = None):
         algo = algo or os.environ.get("TENVEC_B200_ALLREDUCE", "fused")
-        if algo not in ("exact", "nccl", "p2p", "fused"):
+        if algo not in ALGOS:
             raise CollectiveError(f"unknown allreduce algorithm {algo!r}")
-        self._dist = dist
+        self.t = transport if transport is not None else TorchTransport(group)
         self.group = group
-        self.size = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
+        self.size = self.t.size
+        self.rank = self.t.rank
         self.algo = algo
         self.fold = fold or device_fold_strided
         self.counters = [CommCounters() for _ in range(self.size)]
-        self._sym = None  # (uint8 symmetric tensor, handle)
-
-    # -- peer memory (algo="p2p") ---------------------------------------------
-    def _symmetric(self, nbytes: int, device) -> tuple[torch.Tensor, object]:
-        import torch.distributed._symmetric_memory as symm_mem
-
-        if self._sym is None or self._sym[0].numel() < nbytes:
-            name = (self.group or self._dist.group.WORLD).group_name
+        if timeout is None:
             try:
-                symm_mem.enable_symm_mem_for_group(name)
-            except Exception:  # noqa: BLE001 - newer torch enables groups lazily
-                pass
-            cap = max(nbytes, 1 << 20)
-            t = symm_mem.empty(cap, dtype=torch.uint8, device=device)
-            self._sym = (t, symm_mem.rendezvous(t, name))
-        return self._sym
+                timeout = float(os.environ.get("TENVEC_B200_TIMEOUT", "300"))
+            except ValueError:
+                raise CollectiveError("TENVEC_B200_TIMEOUT must be a number of seconds") from None
+        if timeout <= 0:
+            raise CollectiveError("the collective timeout must be positive")
+        self.timeout = float(timeout)
+        self.check = (os.environ.get("TENVEC_B200_CHECK_COLLECTIVES", "0") == "1") if check is None else check
+        # streams of the fused reduction's owner launches (validated up front:
+        # a bad value must not surface after a barrier has been enqueued)
+        self.lanes = _env_int("TENVEC_B200_OWNER_LANES", 2, 1)
+        self._lane_streams: tuple | None = None
+        self._peer: PeerBuffer | None = None
+        self._status: torch.Tensor | None = None  # tv_peer_barrier status block
+        self._epoch_kind: dict[int, str] = {}
+        self._issued = 0
+        self._inflight: collections.deque = collections.deque()
+        self._failed: CollectiveError | None = None
+
+    # -- bookkeeping of issued collectives ------------------------------------
+    def _begin(self, kind: str) -> int:
+        if self._failed is not None:
+            raise self._failed
+        self._issued += 1
+        seq = self._issued
+        if self.check:
+            absent, kinds = self.t.check_kind(self.rank, seq, kind, self.timeout)
+            if absent:
+                raise self._fail(CollectiveTimeout(kind, absent))
+            other = sorted({k for k in kinds.values() if k != kind})
+            if other:
+                raise CollectiveError(f"rank {self.rank} entered {kind!r} while others run {other[0]!r}")
+        return seq
+
+    def _end(self, seq: int, kind: str, on_device: bool) -> None:
+        if not on_device:
+            return
+        ev = torch.cuda.Event()
+        ev.record()
+        self._inflight.append((seq, kind, ev))
+        while len(self._inflight) > 1 and self._inflight[0][2].query():
+            self._inflight.popleft()
+        if len(self._inflight) > 4096:
+            self._inflight.popleft()
+
+    def _fail(self, err: CollectiveError) -> CollectiveError:
+        self._failed = err
+        return err
+
+    def _timed_out(self, seq: int, kind: str) -> CollectiveTimeout:
+        absent = self.t.absent_ranks(self.rank, seq, self._issued, min(self.timeout, 5.0))
+        self.t.abort()
+        return self._fail(CollectiveTimeout(kind, absent if absent is not None else []))
+
+    def _host(self, seq: int, kind: str, fn, *args) -> None:
+        """Run one transport collective, mapping its failures."""
+        try:
+            fn(*args)
+        except CollectiveTimeout as exc:
+            raise self._fail(exc)
+        except CollectiveError:
+            raise
+        except RuntimeError as exc:
+            if self.t.is_timeout(exc):
+                raise self._timed_out(seq, kind) from exc
+            raise CollectiveError(f"{kind}: {exc}") from exc
+
+    def wait(self, timeout: float | None = None) -> None:
+        """Block until every collective this rank issued has completed on the
+        device, giving up when none completes for ``timeout`` seconds
+        (default: the group's).  Raises
+        CollectiveTimeout naming the absent ranks when a device barrier gave
+        up or a collective is still stuck at the deadline."""
+        if self._failed is not None:
+            raise self._failed
+        limit = self.timeout if timeout is None else timeout
+        deadline = time.monotonic() + limit
+        while self._inflight:
+            seq, kind, ev = self._inflight[0]
+            if ev.query():
+                self._inflight.popleft()
+                deadline = time.monotonic() + limit  # progress: the clock restarts
+                continue
+            if time.monotonic() > deadline:
+                raise self._timed_out(seq, kind)
+            time.sleep(0.0005)
+        self._check_status()
+
+    def _check_status(self) -> None:
+        if self._status is None:
+            return
+        st = self._status.cpu().tolist()
+        if st[0] != 0:
+            mask = (st[2] & 0xFFFFFFFF) | ((st[3] & 0xFFFFFFFF) << 32)
+            absent = [r for r in range(self.size) if mask >> r & 1]
+            raise self._fail(CollectiveTimeout(self._epoch_kind.get(st[1], "peer barrier"), absent))
+
+    @contextlib.contextmanager
+    def timeout_scope(self, timeout: float | None):
+        """Temporarily use another timeout (dhopm3(timeout=...))."""
+        if timeout is None:
+            yield self
+            return
+        old = self.timeout
+        self.timeout = float(timeout)
+        try:
+            yield self
+        finally:
+            self.timeout = old
+
+    # -- peer memory -----------------------------------------------------------
+    def _peer_buffer(self, nbytes: int, device) -> PeerBuffer:
+        """This group's peer buffer with at least nbytes of data (collective
+        when it has to grow; raises PeerMemoryUnavailable on every rank)."""
+        if self._peer is not None and self._peer.capacity >= nbytes:
+            return self._peer
+        # the allocation synchronises every rank's device first, so nobody
+        # still reads the buffer being replaced
+        pb = self.t.peer_buffer(max(nbytes, 1 << 20), device)
+        self._peer = pb
+        self._epoch_kind.clear()
+        if self._status is None:
+            self._status = torch.zeros(4, dtype=torch.int32, device=device)
+        return pb
+
+    def _dev_barrier(self, pb: PeerBuffer, kind: str) -> None:
+        pb.epoch += 1
+        self._epoch_kind[pb.epoch] = kind
+        if len(self._epoch_kind) > 4096:
+            self._epoch_kind.pop(next(iter(self._epoch_kind)))
+        lib = _lib.load()
+        _lib.check(lib.tv_peer_barrier(pb.bases_arr, self.size, self.rank, pb.epoch,
+                                       int(self.timeout * 1e9), self._status.data_ptr(),
+                                       _lib.stream_ptr()), f"{kind}: barrier")
 
     def _reduce_p2p(self, buf: torch.Tensor, mixed: bool, mode: PrecisionMode | None,
-                    sizes: list[int]) -> None:
+                    sizes: list[int], seq: int) -> None:
         p, rank = self.size, self.rank
         n, sb = buf.numel(), buf.element_size()
-        sym, hdl = self._symmetric(n * sb, buf.device)
-        mine = as_bits(sym[: n * sb].view(as_bits(buf).dtype))
+        pb = self._peer_buffer(n * sb, buf.device)
+        mine = as_bits(pb.local_data[: n * sb].view(as_bits(buf).dtype))
         mine.copy_(as_bits(buf))
-        ptrs = [int(ptr) for ptr in hdl.buffer_ptrs]
         q = sizes[0]
         lib = _lib.load()
         st, ct = _pair_for(buf, mode)
         stream = _lib.stream_ptr()
-        hdl.barrier(channel=0)                      # every partial is in place
+        self._dev_barrier(pb, "allreduce")           # every partial is in place
         if sizes[rank]:
             off = rank * q * sb
-            srcs = (ctypes.c_void_p * p)(*[ptr + off for ptr in ptrs])
+            srcs = (ctypes.c_void_p * p)(*[pb.data(c) + off for c in range(p)])
             _lib.check(lib.tv_rank_fold(srcs, p, sizes[rank], 0, rank, st, ct, int(mixed),
-                                        ptrs[rank] + off, stream), "p2p fold")
-        hdl.barrier(channel=0)                      # every chunk is reduced
-        srcs = (ctypes.c_void_p * p)(*ptrs)
+                                        pb.data(rank) + off, stream), "p2p fold")
+        self._dev_barrier(pb, "allreduce")           # every chunk is reduced
+        srcs = (ctypes.c_void_p * p)(*[pb.data(c) for c in range(p)])
         _lib.check(lib.tv_rank_select(srcs, p, n, q, st, buf.data_ptr(), stream), "p2p gather")
-        hdl.barrier(channel=0)                      # peers done reading this buffer
+        self._dev_barrier(pb, "allreduce")           # peers done reading this buffer
+        self._end(seq, "allreduce", True)
 
     def _owner_streams(self, device) -> tuple:
-        if getattr(self, "_lanes", None) is None:
-            n = int(os.environ.get("TENVEC_B200_OWNER_LANES", "2"))
-            self._lanes = tuple(torch.cuda.Stream(device=device) for _ in range(max(1, n)))
-        return self._lanes
+        if self._lane_streams is None:
+            self._lane_streams = tuple(torch.cuda.Stream(device=device) for _ in range(self.lanes))
+        return self._lane_streams
 
     def tvc_reduce_fused(self, part, xv: torch.Tensor, k: int, mode: PrecisionMode,
                          counters: list[CommCounters] | None = None,
                          finish_stream: torch.cuda.Stream | None = None) -> torch.Tensor | None:
         """dtvc's split-mode contraction fused with its reduction over peer
-        memory (algo="fused").  The (u, n_k, v) output is cut into p owner
-        ranges -- slab ranges when u >= p, column ranges when u == 1 -- and
-        this rank's TVC launches write range c directly into rank c's receive
-        slot for this rank (a peer pointer: the stores cross NVLink).  After a
-        device barrier the owner folds its p slots (ascending rank / the mixed
-        ring's per-element order, comm.py:84-134, the same bits as every other
-        algorithm), and after a second barrier every rank gathers the p reduced
-        ranges from the owners.  Returns the replicated output, or None when
-        the view has no owner partition (1 < u < p) and the caller falls back.
-        With ``finish_stream`` the fold and gather run there (the caller waits
-        on it before reading the output), overlapping later work."""
+        memory (algo="fused", geometry in ``fused_plan``): this rank's TVC
+        launches write owner range c straight into rank c's receive slot for
+        this rank (a peer pointer: the stores cross NVLink); after a device
+        barrier each owner folds its p slots in the reference's per-element
+        order (ascending rank, or the mixed ring's, comm.py:84-134), and after
+        a second barrier every rank gathers the p reduced ranges from the
+        owners.  The fold is the other transports' fold; the partial sums are
+        those of a TVC over the owner's sub-range, which on integer data (the
+        parity fills) are exact and on float data may round differently from
+        a full-slab launch, within the TVC tolerance.  Returns the replicated
+        output, or None when the view has no owner partition (1 < u < p) or
+        peer memory is unavailable and the caller falls back.  With
+        ``finish_stream`` the fold and gather run there (the caller waits on
+        it before reading the output), overlapping later work."""
+        from .kernels import launch_getvc, launch_tvc
         from .tensor import matricize_dims
 
         p, rank = self.size, self.rank
         md = matricize_dims(part.shape, k)
-        u, nk, v = md.u, md.nk, md.v
-        n = u * v
-        if p == 1 or not (u >= p or u == 1):
+        nk, v = md.nk, md.v
+        plan = fused_plan(md.u, v, p, mode.storage_bytes)
+        if plan is None:
+            return None
+        seq = self._begin("dtvc_reduce")
+        try:
+            pb = self._peer_buffer((p + 1) * plan.slot_bytes, part.buf.device)
+        except PeerMemoryUnavailable as exc:
+            warnings.warn(f"RankGroup: {exc}; using algo='exact'")
+            self.algo = "exact"
+            self._issued -= 1  # the fallback issues its own collective
             return None
         sb = mode.storage_bytes
-        along_u = u >= p
-        outer = u if along_u else v
-        q = -(-outer // p)  # owner c holds outer indices [c q, (c+1) q)
-        unit = v if along_u else 1  # output elements per outer index
-        chunk = q * unit  # output elements per owner (the last one may be short)
-        bounds = [(min(c * q, outer), min((c + 1) * q, outer)) for c in range(p)]
-        sizes = [(b - a) * unit for a, b in bounds]
-        ring = ring_chunks(n, p)
-        slot_bytes = -(-chunk * sb // 16) * 16
-        try:
-            sym, hdl = self._symmetric((p + 1) * slot_bytes, part.buf.device)
-        except Exception as exc:  # noqa: BLE001 - no symmetric memory here: NCCL transport
-            warnings.warn(f"RankGroup: peer memory unavailable ({exc!r:.200}); using algo='exact'")
-            self.algo = "exact"
-            return None
         counters = self.counters if counters is None else counters
         for cc in counters:
             cc.collective_calls += 1
-        _charge_allreduce_movement(counters, [b - a for a, b in ring], p)
-        ptrs = [int(ptr) for ptr in hdl.buffer_ptrs]
+        _charge_allreduce_movement(counters, list(ring_sizes(plan.n, p)), p)
         lib = _lib.load()
         st_, ct_ = mode.tv_storage, mode.tv_compute
         a_ptr = part.buf.data_ptr()
-        hdl.barrier(channel=0)  # peers are done with the previous call's slots
-        # the p owner launches alternate over two streams so one launch's tail
+        self._dev_barrier(pb, "dtvc_reduce")  # peers are done with the previous call's slots
+        # the p owner launches alternate over the lanes so one launch's tail
         # overlaps the next one's ramp (each is a full-GPU grid)
         main = torch.cuda.current_stream()
         lanes = self._owner_streams(part.buf.device)
         for ls in lanes:
             ls.wait_stream(main)
-        for ls in lanes:
             xv.record_stream(ls)
         for j in range(p):  # own range first, then the peers in ring order
             c = (rank + j) % p
-            lo, hi = bounds[c]
+            lo, hi = plan.bounds[c]
             if hi <= lo:
                 continue
-            dst = ptrs[c] + rank * slot_bytes
-            ls = _lib.stream_ptr(lanes[j % len(lanes)])
-            if along_u:
-                rc = lib.tv_tvc(a_ptr + lo * nk * v * sb, st_, ct_, hi - lo, nk, v, xv.data_ptr(),
-                                1.0, 0.0, dst, ls)
+            dst = pb.data(c) + rank * plan.slot_bytes
+            lane = lanes[j % len(lanes)]
+            if plan.along_u:
+                launch_tvc(a_ptr + lo * nk * v * sb, mode, hi - lo, nk, v, xv.data_ptr(), 1.0, 0.0, dst,
+                           part.buf.device, lane, "fused dtvc: contraction into peer memory")
             else:  # u == 1: columns [lo, hi) of the nk x v slab, a strided vecmat
-                rc = lib.tv_getvc(1, a_ptr + lo * sb, st_, ct_, nk, hi - lo, v, xv.data_ptr(),
-                                  1.0, 0.0, dst, ls)
-            _lib.check(rc, "fused dtvc: contraction into peer memory")
+                launch_getvc(1, a_ptr + lo * sb, mode, nk, hi - lo, v, xv.data_ptr(), 1.0, 0.0, dst,
+                             part.buf.device, lane, "fused dtvc: contraction into peer memory")
         for ls in lanes:
             main.wait_stream(ls)
-        out = torch.empty(n, dtype=mode.torch_storage, device=part.buf.device)
+        out = torch.empty(plan.n, dtype=mode.torch_storage, device=part.buf.device)
         if finish_stream is not None:
-            finish_stream.wait_stream(torch.cuda.current_stream())
+            finish_stream.wait_stream(main)
             out.record_stream(finish_stream)
-        with torch.cuda.stream(finish_stream or torch.cuda.current_stream()):
+        with torch.cuda.stream(finish_stream or main):
             stream = _lib.stream_ptr()
-            hdl.barrier(channel=0)  # every slot holds its writer's partial range
-            mine = sizes[rank]
-            if mine:
-                _lib.check(lib.tv_rank_fold_range(sym.data_ptr(), slot_bytes // sb, p, mine,
-                                                  ring[0][1] - ring[0][0], rank * chunk, st_, ct_,
-                                                  int(mode.mixed), sym.data_ptr() + p * slot_bytes,
+            self._dev_barrier(pb, "dtvc_reduce")  # every slot holds its writer's partial range
+            if plan.sizes[rank]:
+                _lib.check(lib.tv_rank_fold_range(pb.data(rank), plan.slot_elems, p, plan.sizes[rank],
+                                                  plan.ring_chunk, rank * plan.chunk, st_, ct_,
+                                                  int(mode.mixed), pb.data(rank) + p * plan.slot_bytes,
                                                   stream), "fused dtvc: owner fold")
-            hdl.barrier(channel=0)  # every owner's reduced range is ready
-            srcs = (ctypes.c_void_p * p)(*[ptrs[c] + p * slot_bytes - c * chunk * sb for c in range(p)])
-            _lib.check(lib.tv_rank_select(srcs, p, n, chunk, st_, out.data_ptr(), stream),
+            self._dev_barrier(pb, "dtvc_reduce")  # every owner's reduced range is ready
+            srcs = (ctypes.c_void_p * p)(*[pb.data(c) + p * plan.slot_bytes - c * plan.chunk * sb
+                                           for c in range(p)])
+            _lib.check(lib.tv_rank_select(srcs, p, plan.n, plan.chunk, st_, out.data_ptr(), stream),
                        "fused dtvc: gather")
+            self._end(seq, "dtvc_reduce", True)
         return out
 
+    # -- host-ordered collectives ----------------------------------------------
     def _check_rank(self, rank: int) -> None:
         if rank != self.rank:
             raise CollectiveError(f"rank {rank} called from process rank {self.rank}")
 
     def barrier(self, rank: int) -> None:
         self._check_rank(rank)
-        self._dist.barrier(group=self.group)
+        seq = self._begin("barrier")
+        self._host(seq, "barrier", self.t.barrier)
 
     def _reduce(self, buf: torch.Tensor, mixed: bool, mode: PrecisionMode | None,
                 counters: list[CommCounters] | None) -> None:
-        p, rank, dist = self.size, self.rank, self._dist
+        p, rank = self.size, self.rank
         n = buf.numel()
-        chunks = ring_chunks(n, p)
-        sizes = [b - a for a, b in chunks]
+        sizes = list(ring_sizes(n, p))
         counters = self.counters if counters is None else counters
+        seq = self._begin("allreduce")
         for c in counters:
             c.collective_calls += 1
         _charge_allreduce_movement(counters, sizes, p)
         if p == 1:
             return
+        t = self.t
         if self.algo == "nccl" and not mixed:
-            dist.all_reduce(buf, group=self.group)
+            self._host(seq, "allreduce", t.all_reduce, buf, "sum")
+            self._end(seq, "allreduce", buf.is_cuda)
             return
         if self.algo == "p2p" and n * buf.element_size() * p > SMALL_GATHER_BYTES:
-            self._reduce_p2p(buf, mixed, mode, sizes)
-            return
+            try:
+                self._reduce_p2p(buf, mixed, mode, sizes, seq)
+                return
+            except PeerMemoryUnavailable as exc:
+                warnings.warn(f"RankGroup: {exc}; using algo='exact'")
+                self.algo = "exact"
         if n * buf.element_size() * p <= SMALL_GATHER_BYTES:
             # latency-bound sizes (dHOPM3 vectors): one all-gather of every
             # rank's buffer, then each rank folds all ring chunks itself --
             # the same values in the same order, one NCCL call instead of two
             everyone = torch.empty(p * n, dtype=buf.dtype, device=buf.device)
-            dist.all_gather_into_tensor(_wire(everyone), _wire(buf.contiguous()), group=self.group)
+            self._host(seq, "allreduce", t.all_gather_into_tensor, _wire(everyone), _wire(buf.contiguous()))
             self.fold(everyone, n, p, n, buf, mixed=mixed, mode=mode, start=0, chunk=sizes[0])
+            self._end(seq, "allreduce", buf.is_cuda)
             return
         mine = sizes[rank]
         recv = torch.empty(p * mine, dtype=buf.dtype, device=buf.device)
-        dist.all_to_all_single(_wire(recv), _wire(buf.contiguous()), output_split_sizes=[mine] * p,
-                               input_split_sizes=sizes, group=self.group)
+        self._host(seq, "allreduce", t.all_to_all_single, _wire(recv), _wire(buf.contiguous()),
+                   [mine] * p, sizes)
         q = sizes[0]
         padded = torch.empty(q, dtype=buf.dtype, device=buf.device)
         if mine:
             self.fold(recv, mine, p, mine, padded[:mine], mixed=mixed, mode=mode, start=rank)
         gathered = torch.empty(p * q, dtype=buf.dtype, device=buf.device)
-        dist.all_gather_into_tensor(_wire(gathered), _wire(padded), group=self.group)
+        self._host(seq, "allreduce", t.all_gather_into_tensor, _wire(gathered), _wire(padded))
         # chunk c sits at [c*q, c*q + sizes[c]); only the tail is short, so the
         # first n gathered elements are the reduced buffer in order
         as_bits(buf).copy_(as_bits(gathered[:n]))
+        self._end(seq, "allreduce", buf.is_cuda)
 
     def all_reduce_sum(self, rank: int, buf: torch.Tensor,
                        counters: list[CommCounters] | None = None) -> None:
@@ -574,26 +768,30 @@ class RankGroup:
         if p == 1 or n == 0 or not buf.is_cuda or self.fold is not device_fold_strided or \
                 (self.algo == "nccl" and not mode.mixed) or n * buf.element_size() * p > SMALL_GATHER_BYTES:
             return False
-        sizes = [b - a for a, b in ring_chunks(n, p)]
+        sizes = list(ring_sizes(n, p))
         counters = self.counters if counters is None else counters
+        seq = self._begin("allreduce")
         for c in counters:
             c.collective_calls += 1
         _charge_allreduce_movement(counters, sizes, p)
         everyone = torch.empty(p * n, dtype=buf.dtype, device=buf.device)
-        self._dist.all_gather_into_tensor(_wire(everyone), _wire(buf.contiguous()), group=self.group)
+        self._host(seq, "allreduce", self.t.all_gather_into_tensor, _wire(everyone), _wire(buf.contiguous()))
         lib = _lib.load()
         sp = status_slot.data_ptr() if status_slot is not None else None
         _lib.check(lib.tv_rank_fold_normalize(everyone.data_ptr(), n, p, n, sizes[0], mode.tv_storage,
                                               mode.tv_compute, int(mode.mixed), dst.data_ptr(),
                                               norm_slot.data_ptr(), sp, counter.data_ptr(),
                                               _lib.stream_ptr()), "allreduce + normalize")
+        self._end(seq, "allreduce", True)
         return True
 
     def raw_all_gather(self, t: torch.Tensor) -> torch.Tensor:
         """Uncounted byte all-gather of equal-length tensors (bookkeeping checks)."""
+        seq = self._begin("all_gather")
         src = t.contiguous().view(torch.uint8)
         out = torch.empty(self.size * src.numel(), dtype=torch.uint8, device=t.device)
-        self._dist.all_gather_into_tensor(out, src, group=self.group)
+        self._host(seq, "all_gather", self.t.all_gather_into_tensor, out, src)
+        self._end(seq, "all_gather", out.is_cuda)
         return out.view(t.dtype)
 
     def all_gather(self, rank: int, local: torch.Tensor, counts: list[int] | None = None
@@ -602,6 +800,7 @@ class RankGroup:
         they differ (the last rank of a split is usually short)."""
         self._check_rank(rank)
         p = self.size
+        seq = self._begin("all_gather")
         for c in self.counters:
             c.collective_calls += 1
         if counts is None:
@@ -613,7 +812,8 @@ class RankGroup:
         padded = torch.empty(q, dtype=local.dtype, device=local.device)
         as_bits(padded[: local.numel()]).copy_(as_bits(local))
         gathered = torch.empty(p * q, dtype=local.dtype, device=local.device)
-        self._dist.all_gather_into_tensor(_wire(gathered), _wire(padded), group=self.group)
+        self._host(seq, "all_gather", self.t.all_gather_into_tensor, _wire(gathered), _wire(padded))
+        self._end(seq, "all_gather", gathered.is_cuda)
         if all(c == q for c in counts):
             return gathered
         parts = [gathered[r * q: r * q + counts[r]] for r in range(p)]

@@ -49,8 +49,12 @@ inline int dtype_bytes(int dt) {
 int set_error(int code, const char* msg);
 int check_launch(const char* what);
 int regime_of(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
+// ws / ws_bytes / ws_given: the split-K workspace (tv_tvc_ws); not given =
+// stream-ordered allocation when the view splits
 int tvc_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                  int64_t su, int64_t sk, const void* x, double alpha, double beta, void* y,
-                 void* stream, int force_generic);
+                 void* stream, int force_generic, void* ws, int64_t ws_bytes, int ws_given);
+int64_t ws_bytes_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
+                          int64_t su, int64_t sk);
 
 }  // namespace tv

@@ -1384,19 +1384,53 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Split-K workspace: caller-provided (tv_tvc_ws / tv_getvc_ws, sized by
+// tv_tvc_workspace_bytes) or, for the plain entry points only, a stream-ordered
+// allocation.  Never a silent fallback to the unsplit kernel: the chunking
+// fixes the summation order, so a view always splits the same way.
+struct Ws {
+  void* p;
+  int64_t bytes;
+  bool given;
+};
+
+// chunk counts of the split-K forms (1 = no split); pure functions of the
+// view so tv_tvc_workspace_bytes can size the workspace ahead of the launch
+static int64_t cols_split(int64_t blocks, int64_t nk) {
+  if (!(blocks < 2LL * sm_count() && nk >= 512)) return 1;
+  const int64_t nch = std::min<int64_t>(cdiv(8LL * sm_count(), blocks), nk / 128);
+  return nch > 1 ? cdiv(nk, cdiv(nk, nch)) : 1;
+}
+
+static int64_t slabs_split(int64_t u, int64_t nk) {
+  if (!(u < 32LL * sm_count() && nk >= 256)) return 1;
+  const int64_t nch = std::min<int64_t>(cdiv(32LL * sm_count(), u), nk / 64);
+  return nch > 1 ? cdiv(nk, cdiv(nk, nch)) : 1;
+}
+
 template <typename C>
-static C* split_alloc(int64_t elems, cudaStream_t st) {
+static C* split_ws(const Ws& ws, int64_t elems, cudaStream_t st, int* rc) {
+  const size_t need = (size_t)elems * sizeof(C);
+  if (ws.given) {
+    if (ws.p == nullptr || ws.bytes < (int64_t)need || (reinterpret_cast<uintptr_t>(ws.p) & 15)) {
+      *rc = set_error(TV_EKERNEL, "tv_tvc: split-K workspace missing, misaligned or smaller than "
+                                  "tv_tvc_workspace_bytes");
+      return nullptr;
+    }
+    return static_cast<C*>(ws.p);
+  }
   void* p = nullptr;
-  if (cudaMallocAsync(&p, (size_t)elems * sizeof(C), st) != cudaSuccess) {
-    cudaGetLastError();  // fall back to the unsplit launch
+  if (cudaMallocAsync(&p, need, st) != cudaSuccess) {
+    cudaGetLastError();
+    *rc = set_error(TV_ECUDA, "tv_tvc: split-K workspace allocation failed (pass one to tv_tvc_ws)");
     return nullptr;
   }
   return static_cast<C*>(p);
 }
 
 template <int SD, typename C>
-static void split_finish(C* ws, int64_t nch, int64_t u, int64_t v, void* y, C al, C be, int hb,
-                         cudaStream_t st) {
+static void split_finish(C* ws, const Ws& given, int64_t nch, int64_t u, int64_t v, void* y, C al, C be,
+                         int hb, cudaStream_t st) {
   using T = typename St<SD>::T;
   const int64_t n = u * v;
   if (nch >= 32) {
@@ -1406,7 +1440,7 @@ static void split_finish(C* ws, int64_t nch, int64_t u, int64_t v, void* y, C al
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8LL * sm_count()));
     k_split_fold<SD, C, false><<<g, 256, 0, st>>>(ws, nch, n, v, (T*)y, al, be, hb);
   }
-  cudaFreeAsync(ws, st);
+  if (!given.given) cudaFreeAsync(ws, st);
 }
 
 template <int SD, typename C>
@@ -1485,33 +1519,44 @@ static void launch_staged_long(const void* A, const void* x, void* y, int64_t u,
   else go(k_staged_long<SD, C, 16>);
 }
 
-template <int SD, typename C, bool AL>
-static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t v,
-                       int64_t su, int64_t sk, C al, C be, int hb, cudaStream_t st) {
+// column blocks of a COLS launch (row phases JR from the view)
+template <int SD, bool AL>
+static int64_t cols_blocks(int64_t u, int64_t nk, int64_t v, int* jr_out, int64_t* ntile_out) {
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
-  constexpr int UA_UNR = VEC >= 8 ? 2 : 4;  // scalar loads in flight: UNR * VEC (8 measured slower)
   const int64_t stripes = cdiv(v, 32 * VEC);
   const int JR = pick_col_phases(nk, stripes, u, AL ? (int)sizeof(T) : 0);
   const int64_t ntile = cdiv(stripes, kWarps / JR);
-  const int64_t blocks = u * ntile;
+  if (jr_out) *jr_out = JR;
+  if (ntile_out) *ntile_out = ntile;
+  return u * ntile;
+}
+
+template <int SD, typename C, bool AL>
+static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t v,
+                       int64_t su, int64_t sk, C al, C be, int hb, const Ws& wsa, cudaStream_t st) {
+  using T = typename St<SD>::T;
+  constexpr int VEC = VecN<SD>::N;
+  constexpr int UA_UNR = VEC >= 8 ? 2 : 4;  // scalar loads in flight: UNR * VEC (8 measured slower)
+  int JR = 1;
+  int64_t ntile = 1;
+  const int64_t blocks = cols_blocks<SD, AL>(u, nk, v, &JR, &ntile);
   if (blocks > 0x7fffffffLL) return set_error(TV_EKERNEL, "tv_tvc: view too large for COLS grid");
   const T* At = (const T*)A;
   const T* xt = (const T*)x;
   T* yt = (T*)y;
   // split-K when the column blocks cannot fill the GPU (< 2 per SM; at 3.2
   // per SM, paper d = 2 k = 0, splitting measured slower: 5.6 vs 5.9 TB/s)
-  int64_t nch = 1;
+  const int64_t nch = cols_split(blocks, nk);
   C* ws = nullptr;
-  if (blocks < 2LL * sm_count() && nk >= 512) {
-    nch = std::min<int64_t>(cdiv(8LL * sm_count(), blocks), nk / 128);
-    if (nch > 1 && (ws = split_alloc<C>(u * nch * v, st)) == nullptr) nch = 1;
+  if (nch > 1) {
+    int rc = TV_OK;
+    if ((ws = split_ws<C>(wsa, u * nch * v, st, &rc)) == nullptr) return rc;
   }
   const int64_t rpc = cdiv(nk, nch);
-  nch = cdiv(nk, rpc);
   const dim3 b((unsigned)blocks, (unsigned)nch);
   auto done = [&]() {
-    if (ws != nullptr) split_finish<SD, C>(ws, nch, u, v, y, al, be, hb, st);
+    if (ws != nullptr) split_finish<SD, C>(ws, wsa, nch, u, v, y, al, be, hb, st);
     return TV_OK;
   };
   // unaligned, fp32/fp64: 3-row batches measured better for 4 row phases
@@ -1538,9 +1583,25 @@ static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t
   }
 }
 
+// split-K workspace bytes tv_tvc needs for this view (0: no split)
+template <int SD, typename C>
+static int64_t ws_bytes_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su, int64_t sk) {
+  using T = typename St<SD>::T;
+  if (u == 0 || v == 0) return 0;
+  int64_t nch = 1;
+  switch (regime_strided(A, (int)sizeof(T), u, nk, v, su, sk)) {
+    case REG_COLS: nch = cols_split(cols_blocks<SD, true>(u, nk, v, nullptr, nullptr), nk); break;
+    case REG_COLS_U: nch = cols_split(cols_blocks<SD, false>(u, nk, v, nullptr, nullptr), nk); break;
+    case REG_SLABS:
+    case REG_SLABS_U: nch = slabs_split(u, nk); break;
+    default: break;
+  }
+  return nch > 1 ? u * nch * v * (int64_t)sizeof(C) : 0;
+}
+
 template <int SD, typename C>
 static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su, int64_t sk,
-                     const void* x, double alpha, double beta, void* y, cudaStream_t st,
+                     const void* x, double alpha, double beta, void* y, const Ws& wsa, cudaStream_t st,
                      int naive) {
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
@@ -1572,10 +1633,10 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       break;
     }
     case REG_COLS:
-      rc = launch_cols<SD, C, true>(A, x, y, u, nk, v, su, sk, al, be, hb, st);
+      rc = launch_cols<SD, C, true>(A, x, y, u, nk, v, su, sk, al, be, hb, wsa, st);
       break;
     case REG_COLS_U:
-      rc = launch_cols<SD, C, false>(A, x, y, u, nk, v, su, sk, al, be, hb, st);
+      rc = launch_cols<SD, C, false>(A, x, y, u, nk, v, su, sk, al, be, hb, wsa, st);
       break;
     case REG_FLAT_ROWS: {
       const int nkv = (int)(nk / VEC);
@@ -1613,14 +1674,10 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
     case REG_SLABS:
     case REG_SLABS_U: {
       // split-K when there are too few slabs for the GPU's warps
-      int64_t nch = 1;
+      const int64_t nch = slabs_split(u, nk);
       C* ws = nullptr;
-      if (u < 32LL * sm_count() && nk >= 256) {
-        nch = std::min<int64_t>(cdiv(32LL * sm_count(), u), nk / 64);
-        if (nch > 1 && (ws = split_alloc<C>(u * nch * v, st)) == nullptr) nch = 1;
-      }
+      if (nch > 1 && (ws = split_ws<C>(wsa, u * nch * v, st, &rc)) == nullptr) return rc;
       const int64_t rpc = cdiv(nk, nch);
-      nch = cdiv(nk, rpc);
       const unsigned grid = grid_for(u * nch, kWarps, 32);
       if (reg == REG_SLABS)
         k_slabs<SD, C, 4, true><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
@@ -1628,7 +1685,7 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       else
         k_slabs<SD, C, 8, false><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
                                                             su, sk, al, be, hb, nch, rpc, ws);
-      if (ws != nullptr) split_finish<SD, C>(ws, nch, u, v, y, al, be, hb, st);
+      if (ws != nullptr) split_finish<SD, C>(ws, wsa, nch, u, v, y, al, be, hb, st);
       break;
     }
     default: {
@@ -1668,21 +1725,34 @@ static int tvc_norm_typed(const void* A, int64_t u, int64_t nk, int64_t v, const
 
 int tvc_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                  int64_t su, int64_t sk, const void* x, double alpha, double beta, void* y,
-                 void* stream, int naive) {
+                 void* stream, int naive, void* ws, int64_t ws_bytes, int ws_given) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Ws w{ws, ws_bytes, ws_given != 0};
   switch (mode_id(storage, compute)) {
     case MODE_F64:
-      return tvc_typed<TV_F64, double>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
+      return tvc_typed<TV_F64, double>(A, u, nk, v, su, sk, x, alpha, beta, y, w, st, naive);
     case MODE_F32:
-      return tvc_typed<TV_F32, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
+      return tvc_typed<TV_F32, float>(A, u, nk, v, su, sk, x, alpha, beta, y, w, st, naive);
     case MODE_F32F64:
-      return tvc_typed<TV_F32, double>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
+      return tvc_typed<TV_F32, double>(A, u, nk, v, su, sk, x, alpha, beta, y, w, st, naive);
     case MODE_F16F32:
-      return tvc_typed<TV_F16, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
+      return tvc_typed<TV_F16, float>(A, u, nk, v, su, sk, x, alpha, beta, y, w, st, naive);
     case MODE_BF16F32:
-      return tvc_typed<TV_BF16, float>(A, u, nk, v, su, sk, x, alpha, beta, y, st, naive);
+      return tvc_typed<TV_BF16, float>(A, u, nk, v, su, sk, x, alpha, beta, y, w, st, naive);
     default:
       return set_error(TV_EMODE, "invalid (storage, compute) pair");
+  }
+}
+
+int64_t ws_bytes_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
+                          int64_t su, int64_t sk) {
+  switch (mode_id(storage, compute)) {
+    case MODE_F64: return ws_bytes_typed<TV_F64, double>(A, u, nk, v, su, sk);
+    case MODE_F32: return ws_bytes_typed<TV_F32, float>(A, u, nk, v, su, sk);
+    case MODE_F32F64: return ws_bytes_typed<TV_F32, double>(A, u, nk, v, su, sk);
+    case MODE_F16F32: return ws_bytes_typed<TV_F16, float>(A, u, nk, v, su, sk);
+    case MODE_BF16F32: return ws_bytes_typed<TV_BF16, float>(A, u, nk, v, su, sk);
+    default: return -1;
   }
 }
 
@@ -1694,7 +1764,25 @@ extern "C" int tv_tvc(const void* A, int storage, int compute, int64_t u, int64_
     return tv::set_error(TV_EKERNEL, "tv_tvc: need u >= 0, nk >= 1, v >= 1");
   if ((u > 0 && (A == nullptr || y == nullptr)) || x == nullptr)
     return tv::set_error(TV_EKERNEL, "tv_tvc: null pointer");
-  return tv::tvc_dispatch(A, storage, compute, u, nk, v, nk * v, v, x, alpha, beta, y, stream, 0);
+  return tv::tvc_dispatch(A, storage, compute, u, nk, v, nk * v, v, x, alpha, beta, y, stream, 0,
+                          nullptr, 0, 0);
+}
+
+extern "C" int tv_tvc_ws(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
+                         const void* x, double alpha, double beta, void* y, void* ws, int64_t ws_bytes,
+                         void* stream) {
+  if (u < 0 || nk < 1 || v < 1)
+    return tv::set_error(TV_EKERNEL, "tv_tvc: need u >= 0, nk >= 1, v >= 1");
+  if ((u > 0 && (A == nullptr || y == nullptr)) || x == nullptr)
+    return tv::set_error(TV_EKERNEL, "tv_tvc: null pointer");
+  return tv::tvc_dispatch(A, storage, compute, u, nk, v, nk * v, v, x, alpha, beta, y, stream, 0,
+                          ws, ws_bytes, 1);
+}
+
+extern "C" int64_t tv_tvc_workspace_bytes(const void* A, int storage, int compute, int64_t u, int64_t nk,
+                                          int64_t v) {
+  if (u < 0 || nk < 1 || v < 1) return -1;
+  return tv::ws_bytes_dispatch(A, storage, compute, u, nk, v, nk * v, v);
 }
 
 extern "C" int tv_tvc_naive(const void* A, int storage, int compute, int64_t u, int64_t nk,
@@ -1704,7 +1792,8 @@ extern "C" int tv_tvc_naive(const void* A, int storage, int compute, int64_t u, 
     return tv::set_error(TV_EKERNEL, "tv_tvc_naive: need u >= 0, nk >= 1, v >= 1");
   if ((u > 0 && (A == nullptr || y == nullptr)) || x == nullptr)
     return tv::set_error(TV_EKERNEL, "tv_tvc_naive: null pointer");
-  return tv::tvc_dispatch(A, storage, compute, u, nk, v, nk * v, v, x, alpha, beta, y, stream, 1);
+  return tv::tvc_dispatch(A, storage, compute, u, nk, v, nk * v, v, x, alpha, beta, y, stream, 1,
+                          nullptr, 0, 0);
 }
 
 extern "C" int tv_tvc_normalize(const void* A, int storage, int compute, int64_t u, int64_t nk,
@@ -1736,19 +1825,41 @@ extern "C" int tv_set_regime_override(int regime) {
   return prev;
 }
 
-extern "C" int tv_getvc(int trans, const void* A, int storage, int compute, int64_t m, int64_t n,
-                        int64_t lda, const void* x, double alpha, double beta, void* y,
-                        void* stream) {
+static int getvc_impl(int trans, const void* A, int storage, int compute, int64_t m, int64_t n,
+                      int64_t lda, const void* x, double alpha, double beta, void* y, void* stream,
+                      void* ws, int64_t ws_bytes, int given) {
   if (m < 0 || n < 0 || lda < n) return tv::set_error(TV_EKERNEL, "tv_getvc: need lda >= n >= 0");
   if (trans == 0) {  // matvec: y[i] = sum_j A[i*lda + j] x[j]
     if (m == 0) return TV_OK;
     if (n == 0) return tv::set_error(TV_EKERNEL, "tv_getvc: empty contraction");
-    return tv::tvc_dispatch(A, storage, compute, m, n, 1, lda, 1, x, alpha, beta, y, stream, 0);
+    return tv::tvc_dispatch(A, storage, compute, m, n, 1, lda, 1, x, alpha, beta, y, stream, 0, ws,
+                            ws_bytes, given);
   }
   if (trans == 1) {  // vecmat: y[c] = sum_i x[i] A[i*lda + c]
     if (n == 0) return TV_OK;
     if (m == 0) return tv::set_error(TV_EKERNEL, "tv_getvc: empty contraction");
-    return tv::tvc_dispatch(A, storage, compute, 1, m, n, 0, lda, x, alpha, beta, y, stream, 0);
+    return tv::tvc_dispatch(A, storage, compute, 1, m, n, 0, lda, x, alpha, beta, y, stream, 0, ws,
+                            ws_bytes, given);
   }
   return tv::set_error(TV_EKERNEL, "tv_getvc: trans must be 0 (matvec) or 1 (vecmat)");
+}
+
+extern "C" int tv_getvc(int trans, const void* A, int storage, int compute, int64_t m, int64_t n,
+                        int64_t lda, const void* x, double alpha, double beta, void* y,
+                        void* stream) {
+  return getvc_impl(trans, A, storage, compute, m, n, lda, x, alpha, beta, y, stream, nullptr, 0, 0);
+}
+
+extern "C" int tv_getvc_ws(int trans, const void* A, int storage, int compute, int64_t m, int64_t n,
+                           int64_t lda, const void* x, double alpha, double beta, void* y, void* ws,
+                           int64_t ws_bytes, void* stream) {
+  return getvc_impl(trans, A, storage, compute, m, n, lda, x, alpha, beta, y, stream, ws, ws_bytes, 1);
+}
+
+extern "C" int64_t tv_getvc_workspace_bytes(int trans, const void* A, int storage, int compute, int64_t m,
+                                            int64_t n, int64_t lda) {
+  if (m < 0 || n < 0 || lda < n) return -1;
+  if (trans == 0) return m == 0 || n == 0 ? 0 : tv::ws_bytes_dispatch(A, storage, compute, m, n, 1, lda, 1);
+  if (trans == 1) return m == 0 || n == 0 ? 0 : tv::ws_bytes_dispatch(A, storage, compute, 1, m, n, 0, lda);
+  return -1;
 }

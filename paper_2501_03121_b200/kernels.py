@@ -85,6 +85,42 @@ def _vec(x, mode: PrecisionMode, what: str) -> torch.Tensor:
     return t.contiguous()
 
 
+def _workspace(nbytes: int, device, stream: torch.cuda.Stream | None) -> tuple[int, int, object]:
+    """Split-K workspace for one launch from torch's caching allocator
+    (stream-ordered, captured into graph pools, no driver allocation)."""
+    if nbytes <= 0:
+        return 0, 0, None
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    if stream is not None and stream != torch.cuda.current_stream(device):
+        ws.record_stream(stream)
+    return ws.data_ptr(), nbytes, ws
+
+
+def launch_tvc(a_ptr: int, mode: PrecisionMode, u: int, nk: int, v: int, x_ptr: int, alpha: float,
+               beta: float, y_ptr: int, device, stream: torch.cuda.Stream | None = None,
+               what: str = "tvc_native") -> None:
+    """tv_tvc_ws over the contiguous (u, nk, v) view at a_ptr, with the
+    split-K workspace it asks for (tv_tvc_workspace_bytes)."""
+    lib = _lib.load()
+    need = lib.tv_tvc_workspace_bytes(a_ptr, mode.tv_storage, mode.tv_compute, u, nk, v)
+    wp, wb, keep = _workspace(need, device, stream)
+    _lib.check(lib.tv_tvc_ws(a_ptr, mode.tv_storage, mode.tv_compute, u, nk, v, x_ptr, float(alpha),
+                             float(beta), y_ptr, wp, wb, _lib.stream_ptr(stream)), what)
+    del keep
+
+
+def launch_getvc(trans: int, a_ptr: int, mode: PrecisionMode, m: int, n: int, lda: int, x_ptr: int,
+                 alpha: float, beta: float, y_ptr: int, device, stream: torch.cuda.Stream | None = None,
+                 what: str = "getvc") -> None:
+    """tv_getvc_ws with its split-K workspace (tv_getvc_workspace_bytes)."""
+    lib = _lib.load()
+    need = lib.tv_getvc_workspace_bytes(trans, a_ptr, mode.tv_storage, mode.tv_compute, m, n, lda)
+    wp, wb, keep = _workspace(need, device, stream)
+    _lib.check(lib.tv_getvc_ws(trans, a_ptr, mode.tv_storage, mode.tv_compute, m, n, lda, x_ptr,
+                               float(alpha), float(beta), y_ptr, wp, wb, _lib.stream_ptr(stream)), what)
+    del keep
+
+
 def getvc(
     trans: str,
     alpha: float,
@@ -127,10 +163,8 @@ def getvc(
     xv = _vec(x, mode, "x")
     if y.stride(0) != 1:
         raise KernelError("y must be contiguous")
-    lib = _lib.load()
-    _lib.check(lib.tv_getvc(code, a.data_ptr(), mode.tv_storage, mode.tv_compute, m, n, max(lda, n),
-                            xv.data_ptr(), float(alpha), float(beta), y.data_ptr(),
-                            _lib.stream_ptr()), "getvc")
+    launch_getvc(code, a.data_ptr(), mode, m, n, max(lda, n), xv.data_ptr(), alpha, beta, y.data_ptr(),
+                 y.device)
     if counters is not None:
         read = m * n + in_len + (out_len if beta != 0.0 else 0)
         counters.count("getvc", read, out_len, mode.storage_bytes)
@@ -164,10 +198,8 @@ def tvc_native(
         raise KernelError("out must be a CUDA tensor in the storage format")
     ybuf = out[:out_size]
     xv = _vec(x, mode, "x")
-    lib = _lib.load()
-    _lib.check(lib.tv_tvc(t.buf.data_ptr(), mode.tv_storage, mode.tv_compute, md.u, md.nk, md.v,
-                          xv.data_ptr(), float(alpha), float(beta), ybuf.data_ptr(),
-                          _lib.stream_ptr()), "tvc_native")
+    launch_tvc(t.buf.data_ptr(), mode, md.u, md.nk, md.v, xv.data_ptr(), alpha, beta, ybuf.data_ptr(),
+               t.device)
     if counters is not None:
         read = t.size + md.nk + (out_size if beta != 0.0 else 0)
         counters.count("tvc", read, out_size, mode.storage_bytes)

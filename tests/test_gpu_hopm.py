@@ -415,3 +415,20 @@ def test_dhopm3_graph_replay_equals_eager(tv):
         assert eager.tvc_count == graph.tvc_count
         assert eager.kernel_counters[0] == graph.kernel_counters[0]
         assert eager.comm_counters[0] == graph.comm_counters[0]
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_dhopm3_order4_fp64_split3_twenty_sweeps_96(tv, oracle, p):
+    """C4's code path scaled to 96^4: order-4 fp64, split s = 3,
+    20 sweeps, p in-process ranks -- vectors and every lambda within 1e-12 of
+    the oracle run of the same split (hopm.py:229-354)."""
+    O = oracle
+    shape = (96,) * 4
+    vals = O.fill_values(shape, "hash", seed=1).reshape(shape)
+    x0 = O.initial_vectors(shape, "f64")
+    res = tv.dhopm3(tv.distribute(tv.Tensor.from_array(vals), 3, p), [v.copy() for v in x0], sweeps=20)
+    vecs, norms = O.dhopm3(vals, 3, p, x0, 20, "f64")
+    assert len(res.norms) == 20
+    np.testing.assert_allclose(np.asarray(res.norms), np.asarray(norms), rtol=1e-12, atol=0)
+    for got, want in zip(res.vectors, vecs):
+        assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)

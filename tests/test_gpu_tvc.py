@@ -359,3 +359,36 @@ def test_getvc_tall_strided_views_split_k(tv):
     yw = torch.full((257,), 3.0, dtype=torch.float64, device="cuda")
     tv.getvc(tv.VECMAT, 1.0, wide, xw, 0.5, yw)
     assert torch.equal(yw, xw @ wide + 1.5)
+
+
+@pytest.mark.parametrize("shape,k", [((4, 4096, 4096), 1), ((1, 1 << 20, 3), 1), ((1 << 16, 8), 0)])
+def test_split_k_workspace_is_caller_provided(tv, oracle, shape, k):
+    """Views with few, long outputs split the rows into chunks; the chunk
+    count is a pure function of the view (tv_tvc_workspace_bytes), the
+    workspace comes from the caller (tv_tvc_ws), a short one is an error, not
+    a silent switch to another kernel, and every path gives the same bits."""
+    import torch
+    from paper_2501_03121_b200 import _lib
+
+    O = oracle
+    lib = _lib.load()
+    vals = O.fill_values(shape, "hash", seed=5)
+    t = tv.Tensor.from_array(vals.reshape(shape))
+    md = tv.matricize_dims(t.shape, k)
+    x = torch.from_numpy((np.arange(shape[k]) % 7) + 1.0).cuda()
+    need = lib.tv_tvc_workspace_bytes(t.buf.data_ptr(), 0, 0, md.u, md.nk, md.v)
+    assert need > 0
+    y_ws = torch.empty(md.u * md.v, dtype=torch.float64, device="cuda")
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    st = _lib.stream_ptr()
+    assert lib.tv_tvc_ws(t.buf.data_ptr(), 0, 0, md.u, md.nk, md.v, x.data_ptr(), 1.0, 0.0, y_ws.data_ptr(),
+                         ws.data_ptr(), need - 16, st) == 1
+    assert lib.tv_tvc_ws(t.buf.data_ptr(), 0, 0, md.u, md.nk, md.v, x.data_ptr(), 1.0, 0.0, y_ws.data_ptr(),
+                         ws.data_ptr(), need, st) == 0
+    y_plain = torch.empty_like(y_ws)
+    assert lib.tv_tvc(t.buf.data_ptr(), 0, 0, md.u, md.nk, md.v, x.data_ptr(), 1.0, 0.0, y_plain.data_ptr(),
+                      st) == 0
+    y_api = tv.tvc_native(t, x.cpu().numpy(), k).buf
+    want = O.tvc(vals, shape, x.cpu().numpy(), k, "f64")
+    for y in (y_ws, y_plain, y_api):
+        assert np.array_equal(y.cpu().numpy(), want)

@@ -145,7 +145,7 @@ def test_worker_group_rendezvous_errors():
 
 def _header_symbols() -> set[str]:
     text = (ROOT / "include" / "tenvec_b200.h").read_text()
-    return set(re.findall(r"^\s*(?:const char\*|int)\s+(tv_\w+)\s*\(", text, flags=re.M))
+    return set(re.findall(r"^\s*(?:const char\*|int64_t|int)\s+(tv_\w+)\s*\(", text, flags=re.M))
 
 
 def test_library_builds_loads_and_exports_every_header_symbol():
@@ -210,3 +210,28 @@ def test_no_oracle_import_in_product():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "tenvec_oracle" not in text and "oracle/" not in text, f
+
+
+class _FakeTransport:
+    size, rank, backend, store = 2, 0, "fake", None
+
+
+def test_rank_group_validates_knobs_up_front(monkeypatch):
+    """A malformed TENVEC_B200_OWNER_LANES / timeout fails at construction,
+    before any barrier could be enqueued (comm.py _owner_streams)."""
+    from paper_2501_03121_b200 import RankGroup
+    from paper_2501_03121_b200.errors import CollectiveError
+
+    monkeypatch.setenv("TENVEC_B200_OWNER_LANES", "two")
+    with pytest.raises(CollectiveError):
+        RankGroup(transport=_FakeTransport())
+    monkeypatch.setenv("TENVEC_B200_OWNER_LANES", "0")
+    with pytest.raises(CollectiveError):
+        RankGroup(transport=_FakeTransport())
+    monkeypatch.setenv("TENVEC_B200_OWNER_LANES", "3")
+    g = RankGroup(transport=_FakeTransport(), timeout=5)
+    assert g.lanes == 3 and g.size == 2 and g.timeout == 5.0
+    with pytest.raises(CollectiveError):
+        RankGroup(transport=_FakeTransport(), timeout=0)
+    with pytest.raises(CollectiveError):
+        RankGroup(transport=_FakeTransport(), algo="ring")

@@ -98,3 +98,67 @@ def test_rank_group_reference_values_over_gloo(world):
         assert p.exitcode == 0
     for r in range(world):
         assert all(out[r]), (r, out[r])
+
+
+def _failure_worker(rank, world, port, q, scenario):
+    import datetime
+
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=3))
+    import paper_2501_03121_b200 as tv
+
+    try:
+        if scenario == "absent":
+            g = tv.RankGroup(algo="exact", timeout=2.0)
+            if rank == world - 1:
+                import time
+
+                time.sleep(9)
+                q.put((rank, "slept"))
+                return
+            try:
+                g.all_gather(rank, torch.ones(3, dtype=torch.float64))
+                q.put((rank, "no error"))
+            except tv.CollectiveTimeout as exc:
+                try:
+                    g.barrier(rank)
+                    again = False
+                except tv.CollectiveTimeout as exc2:
+                    again = exc2 is exc
+                q.put((rank, (exc.kind, exc.absent, again)))
+        else:  # mismatched collective kinds under check=True
+            g = tv.RankGroup(algo="exact", check=True, timeout=20.0)
+            buf = torch.ones(8, dtype=torch.float64)
+            try:
+                g.all_reduce_sum(rank, buf) if rank == 0 else g.all_gather(rank, buf)
+                q.put((rank, "no error"))
+            except tv.CollectiveError as exc:
+                q.put((rank, (type(exc).__name__, "while others run" in str(exc))))
+    finally:
+        q.close()
+        q.join_thread()  # flush the result before leaving
+        os._exit(0)  # skip the teardown handshake with a peer that may be gone
+
+
+@pytest.mark.parametrize("scenario", ["absent", "mismatch"])
+def test_rank_group_failure_semantics_over_gloo(scenario):
+    """CollectiveTimeout names the ranks that never issued the collective
+    (a ledger in the c10d store) and the group stays failed; with check=True
+    a kind mismatch raises CollectiveError on every rank (comm.py:206-235)."""
+    world = 3 if scenario == "absent" else 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_failure_worker, args=(r, world, port, q, scenario)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    if scenario == "absent":
+        assert out[world - 1] == "slept"
+        for r in range(world - 1):
+            assert out[r] == ("all_gather", [world - 1], True), out
+    else:
+        assert out == {0: ("CollectiveError", True), 1: ("CollectiveError", True)}, out
