@@ -219,6 +219,13 @@ int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t chunk, int
 int tv_peer_barrier(void* const* peer_bases, int p, int rank, uint32_t epoch, int64_t timeout_ns,
                     int32_t* status, void* stream);
 
+/* Load every kernel of the library into the current device's context now
+ * (CUDA 12 loads kernels lazily, at first launch, and a load may wait for the
+ * kernels already running -- including a tv_peer_barrier that waits for this
+ * rank: call it before the first barrier).  *loaded (may be NULL) receives
+ * the number of kernels loaded. */
+int tv_preload(int* loaded);
+
 /* Fill the rank-local slab [s_lo, s_hi) along mode s of a global tensor with
  * extents ext[0..d-1] (last mode fastest) from the GLOBAL linear index g:
  * ones -> 1, ramp -> (g mod 97) + 1, hash -> (splitmix64(seed, g) mod 97) + 1. */

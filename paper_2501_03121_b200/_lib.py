@@ -58,6 +58,7 @@ SIGNATURES = {
     "tv_rank_fold_range": (_int, [_vp, _i64, _int, _i64, _i64, _i64, _int, _int, _int, _vp, _vp]),
     "tv_rank_select": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp]),
     "tv_peer_barrier": (_int, [ctypes.POINTER(_vp), _int, _int, ctypes.c_uint32, _i64, _vp, _vp]),
+    "tv_preload": (_int, [ctypes.POINTER(_int)]),
     "tv_fill": (_int, [_vp, _int, _int, ctypes.c_uint64, ctypes.POINTER(_i64), _int, _int, _i64, _i64, _vp]),
     "tv_axpby": (_int, [ctypes.c_double, _vp, ctypes.c_double, _vp, _int, _int, _i64, _vp]),
     "tv_read_stream": (_int, [_vp, _i64, _vp, _vp]),
@@ -90,6 +91,50 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         if path is None:
             _lib = lib
         return lib
+
+
+_preloaded: set = set()
+
+
+def preload() -> int:
+    """tv_preload on the current device, once per device: every kernel loaded
+    before a device barrier can spin (lazy loading could otherwise make a
+    first launch wait for the barrier that waits for it)."""
+    import torch
+
+    dev = torch.cuda.current_device()
+    if dev in _preloaded:
+        return 0
+    lib = load()
+    n = ctypes.c_int(0)
+    check(lib.tv_preload(ctypes.byref(n)), "tv_preload")
+    with _lock:
+        _preloaded.add(dev)
+    return n.value
+
+
+def host_wait(stream=None) -> None:
+    """Wait on the host for the work queued on ``stream`` (default: the
+    current one) by polling an event, never inside a blocking driver call:
+    thread-ranks sharing one GPU (loopback) keep issuing work -- the very
+    barrier arrival this stream may be waiting for -- while this one waits,
+    and a blocking synchronize can hold driver locks their calls need."""
+    import time
+
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    ev = torch.cuda.Event()
+    ev.record(s)
+    while not ev.query():
+        time.sleep(5e-5)
+
+
+def to_host(t):
+    """t.cpu() after host_wait()."""
+    if t.is_cuda:
+        host_wait()
+    return t.cpu()
 
 
 def check(rc: int, what: str = "") -> None:

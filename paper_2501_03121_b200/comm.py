@@ -552,7 +552,10 @@ class RankGroup:
         if self._peer is not None and self._peer.capacity >= nbytes:
             return self._peer
         # the allocation synchronises every rank's device first, so nobody
-        # still reads the buffer being replaced
+        # still reads the buffer being replaced; every kernel is loaded before
+        # the first barrier can spin
+        with torch.cuda.device(device):
+            _lib.preload()
         pb = self.t.peer_buffer(max(nbytes, 1 << 20), device)
         self._peer = pb
         self._epoch_kind.clear()

@@ -15,6 +15,7 @@
 // peer costs one timeout, not one per barrier, and the host raises
 // CollectiveTimeout(kind, absent) when it reads the status.
 
+#include <cuda.h>
 #include <stdint.h>
 
 #include "tv_internal.h"
@@ -96,4 +97,65 @@ extern "C" int tv_peer_barrier(void* const* peer_bases, int p, int rank, uint32_
   k_peer_barrier<<<1, TV_MAX_RANKS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       w, p, rank, epoch, (long long)timeout_ns, status);
   return check_launch("tv_peer_barrier");
+}
+
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first
+// launch, and loading may wait for the kernels already running on the device.
+// A kernel first launched while a tv_peer_barrier spins -- on this GPU for a
+// side-stream barrier, or for a peer thread-rank sharing the GPU -- would then
+// wait for the barrier, which waits for it.  tv_preload loads every kernel of
+// every translation unit up front (driver entry points of CUDA >= 12.4, looked
+// up at run time: no link against libcuda).
+namespace {
+using PFuncGetModule = CUresult (*)(CUmodule*, CUfunction);
+using PModFnCount = CUresult (*)(unsigned*, CUmodule);
+using PModEnum = CUresult (*)(CUfunction*, unsigned, CUmodule);
+using PFuncLoad = CUresult (*)(CUfunction);
+
+template <typename F>
+F entry(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion(name, &fn, 12040, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return reinterpret_cast<F>(fn);
+}
+}  // namespace
+
+extern "C" int tv_preload(int* loaded) {
+  using namespace tv;
+  const void* anchors[3] = {anchor_tvc(), anchor_util(), reinterpret_cast<const void*>(&k_peer_barrier)};
+  auto get_mod = entry<PFuncGetModule>("cuFuncGetModule");
+  auto count = entry<PModFnCount>("cuModuleGetFunctionCount");
+  auto enumerate = entry<PModEnum>("cuModuleEnumerateFunctions");
+  auto load = entry<PFuncLoad>("cuFuncLoad");
+  int n_loaded = 0;
+  for (const void* a : anchors) {
+    cudaFunction_t f = nullptr;
+    if (cudaGetFuncBySymbol(&f, a) != cudaSuccess) return check_launch("tv_preload: cudaGetFuncBySymbol");
+    if (!get_mod || !count || !enumerate || !load) {
+      // driver without the enumeration API: the anchors at least
+      cudaFuncAttributes attr;
+      if (cudaFuncGetAttributes(&attr, a) != cudaSuccess) return check_launch("tv_preload");
+      ++n_loaded;
+      continue;
+    }
+    CUmodule mod = nullptr;
+    unsigned nf = 0;
+    if (get_mod(&mod, reinterpret_cast<CUfunction>(f)) != CUDA_SUCCESS || count(&nf, mod) != CUDA_SUCCESS)
+      return set_error(TV_ECUDA, "tv_preload: cannot enumerate the module's kernels");
+    CUfunction fs[1024];
+    if (nf > 1024) return set_error(TV_ECUDA, "tv_preload: more than 1024 kernels in one module");
+    if (enumerate(fs, nf, mod) != CUDA_SUCCESS)
+      return set_error(TV_ECUDA, "tv_preload: cannot enumerate the module's kernels");
+    for (unsigned i = 0; i < nf; ++i) {
+      if (load(fs[i]) != CUDA_SUCCESS) return set_error(TV_ECUDA, "tv_preload: cuFuncLoad failed");
+      ++n_loaded;
+    }
+  }
+  if (loaded) *loaded = n_loaded;
+  return TV_OK;
 }

@@ -54,6 +54,9 @@ int regime_of(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
 int tvc_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                  int64_t su, int64_t sk, const void* x, double alpha, double beta, void* y,
                  void* stream, int force_generic, void* ws, int64_t ws_bytes, int ws_given);
+// one kernel of each translation unit (tv_preload finds its module)
+const void* anchor_tvc();
+const void* anchor_util();
 int64_t ws_bytes_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                           int64_t su, int64_t sk);
 

@@ -1744,6 +1744,8 @@ int tvc_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk,
   }
 }
 
+const void* anchor_tvc() { return reinterpret_cast<const void*>(&k_naive_rows<TV_F64, double>); }
+
 int64_t ws_bytes_dispatch(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
                           int64_t su, int64_t sk) {
   switch (mode_id(storage, compute)) {

@@ -361,6 +361,8 @@ __global__ void __launch_bounds__(256) k_read_stream(const uint4* __restrict__ p
   if (acc == 0x9E3779B9u) sink[0] = acc;
 }
 
+const void* anchor_util() { return reinterpret_cast<const void*>(&k_read_stream); }
+
 }  // namespace tv
 
 // ================================================================ C-ABI ====

@@ -268,7 +268,7 @@ def tvc_looped_oracle(t: Tensor, x, k: int) -> np.ndarray:
     _lib.check(lib.tv_tvc_naive(a64.data_ptr(), _lib.TV_F64, _lib.TV_F64, md.u, md.nk, md.v,
                                 x64.data_ptr(), 1.0, 0.0, y.data_ptr(), _lib.stream_ptr()),
                "tvc_looped_oracle")
-    return y.cpu().numpy().reshape(t.shape.drop(k).extents)
+    return _lib.to_host(y).numpy().reshape(t.shape.drop(k).extents)
 
 
 def axpby(
@@ -296,7 +296,7 @@ def axpby(
     _lib.check(lib.tv_axpby(float(alpha), xv.data_ptr(), float(beta), yv.data_ptr(), mode.tv_storage,
                             mode.tv_compute, yv.numel(), _lib.stream_ptr()), "axpby")
     if host is not None:
-        host[...] = yv.cpu().numpy()
+        host[...] = _lib.to_host(yv).numpy()
     if counters is not None:
         n = yv.numel()
         counters.count("axpby", n + (n if beta != 0.0 else 0), n, mode.storage_bytes)
@@ -327,7 +327,7 @@ def norm2(x, *, mode: PrecisionMode = F64, counters: KernelCounters | None = Non
     _norm_async(xv, mode, slot, None, scale=False)
     if counters is not None:
         counters.count("norm2", xv.numel(), 0, mode.storage_bytes)
-    return float(slot.item())
+    return float(_lib.to_host(slot).item())
 
 
 def normalize(x, *, mode: PrecisionMode = F64, counters: KernelCounters | None = None) -> float:
@@ -342,10 +342,10 @@ def normalize(x, *, mode: PrecisionMode = F64, counters: KernelCounters | None =
     _norm_async(xv, mode, slot, status, scale=True)
     if counters is not None:
         counters.count("norm2", xv.numel(), 0, mode.storage_bytes)
-    if int(status.item()) != 0:
+    if int(_lib.to_host(status).item()) != 0:
         raise NormalizationError("cannot normalize a zero vector")
     if counters is not None:
         counters.count("scale", xv.numel(), xv.numel(), mode.storage_bytes)
     if host is not None:
-        host[...] = xv.cpu().numpy()
-    return float(slot.item())
+        host[...] = _lib.to_host(xv).numpy()
+    return float(_lib.to_host(slot).item())

@@ -16,17 +16,27 @@ per call, with the reference's timeout and kind checks), each rank's stream
 waits for its peers' events and copies, and a second meeting keeps inputs
 alive until every peer has read them.
 
+Two rules keep p ranks on one GPU from deadlocking on the spinning device
+barrier: host waits poll an event (``_lib.host_wait``) instead of blocking in
+the driver, and every stream gets its own hardware queue --
+CUDA_DEVICE_MAX_CONNECTIONS (default 8) must cover the ranks' streams (about
+5 per rank: its own, two owner lanes, two side streams), so set it to 32
+before the CUDA context exists (tests/conftest.py does).
+
 Used by the ``-m gpu`` tests to cover the multi-GPU transports on a one-GPU
 box; also a debugging tool (a p-rank run needs one GPU).
 """
 
 from __future__ import annotations
 
+import os
 import threading
 import time
+import warnings
 
 import torch
 
+from . import _lib
 from .errors import CollectiveError, CollectiveTimeout
 from .transport import TV_PEER_HEADER, PeerBuffer, PeerMemoryUnavailable
 
@@ -59,6 +69,11 @@ class LoopbackWorld:
         self._meets: dict[int, _Meet] = {}
         self._calls = [0] * size
         self.issued = [0] * size  # collectives issued per rank (the ledger)
+        conns = int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8") or 8)
+        if 5 * size > conns:
+            warnings.warn(f"LoopbackWorld({size}): CUDA_DEVICE_MAX_CONNECTIONS={conns} < {5 * size}; "
+                          "streams of different thread-ranks may share a hardware queue and a device "
+                          "barrier can then wait for work queued behind it (set it to 32 before CUDA starts)")
 
     def transport(self, rank: int) -> "LoopbackTransport":
         return LoopbackTransport(self, rank)
@@ -115,7 +130,7 @@ class LoopbackWorld:
                 s.wait_stream(main)
                 with torch.cuda.stream(s):
                     results[r] = fn(r, self.transport(r), *args)
-                s.synchronize()
+                _lib.host_wait(s)
             except BaseException as exc:  # noqa: BLE001
                 errors[r] = exc
 
@@ -204,7 +219,7 @@ class LoopbackTransport:
     def peer_buffer(self, nbytes: int, device) -> PeerBuffer:
         ok = self.rank != self.world.fail_peer_rank
         local = torch.zeros(TV_PEER_HEADER + nbytes, dtype=torch.uint8, device=device) if ok else None
-        torch.cuda.current_stream().synchronize()  # headers are zero before any peer posts
+        _lib.host_wait()  # headers are zero before any peer posts
         everyone = self.world.meet(self.rank, "peer_buffer", local)
         if any(t is None for t in everyone):
             raise PeerMemoryUnavailable("peer memory: allocate failed on another rank"

@@ -162,7 +162,7 @@ def _roundtrip(a, fn):
     if isinstance(a, torch.Tensor):
         return fn(_to_device(a))
     res = fn(_to_device(a, np_brain=True))
-    return res.cpu().numpy()
+    return _lib.to_host(res).numpy()
 
 
 def f32_to_bf16_bits(a):

@@ -1,5 +1,11 @@
+import os
 import sys
 from pathlib import Path
+
+# before any CUDA context exists: one hardware queue per stream, so the
+# loopback tests' thread-ranks (each with its own streams on one GPU) never
+# queue a kernel behind another rank's spinning device barrier
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import numpy as np
 import pytest

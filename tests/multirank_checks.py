@@ -19,6 +19,8 @@ import threading
 import numpy as np
 import torch
 
+from paper_2501_03121_b200._lib import to_host
+
 _CACHE: dict = {}
 _LOCK = threading.Lock()
 
@@ -97,7 +99,7 @@ def run_checks(rank: int, world: int, make_group, tv, O, *, quick: bool = False)
     rag = torch.arange(1, 300_003, dtype=torch.float32, device="cuda") * (rank + 1)
     want = torch.arange(1, 300_003, dtype=torch.float32) * sum(r + 1 for r in range(world))
     p2p.all_reduce_sum(rank, rag)
-    ok.append(("f32", "ragged-p2p", 0, bool(torch.equal(rag.cpu(), want))))
+    ok.append(("f32", "ragged-p2p", 0, bool(torch.equal(to_host(rag), want))))
 
     # the split-mode contraction fused with its reduction over peer memory
     # (algo="fused"): slab-range owners (u >= p, a ragged / empty last
@@ -181,8 +183,8 @@ def run_checks(rank: int, world: int, make_group, tv, O, *, quick: bool = False)
             slot = torch.empty(1, dtype=torch.float64, device="cuda")
             cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
             okf = group.all_reduce_normalize(rank, v, mode, dst, slot, None, cnt)
-            same = bool(torch.equal(as_i(dst), as_i(ref)))
-            ok.append((name, "fold-normalize", n, okf and same and float(slot.item()) == ref_norm))
+            same = bool(torch.equal(to_host(as_i(dst)), to_host(as_i(ref))))
+            ok.append((name, "fold-normalize", n, okf and same and float(to_host(slot).item()) == ref_norm))
 
     # dhopm3 across the group: bit-identical to the in-process run of the
     # same split (the reference's threads-as-ranks model) and within

@@ -17,6 +17,7 @@ import pytest
 import torch
 
 import multirank_checks
+from paper_2501_03121_b200._lib import to_host
 
 pytestmark = pytest.mark.gpu
 
@@ -225,10 +226,10 @@ def test_c3_full_size_dtvc_split_mode_sampled(tv):
         res = {}
         for k in range(5):
             if k == s:
-                res[k] = out[k].parts[0].buf[torch.from_numpy(idx[k]).cuda()].cpu().numpy()
+                res[k] = to_host(out[k].parts[0].buf[torch.from_numpy(idx[k]).cuda()]).numpy()
         # the ranks own slabs of the k != s outputs along the split mode
         # (now mode 3); rank 0 checks its own outputs' samples
-        return res, {k: out[k].parts[rank].buf.cpu().numpy() if k != s else None for k in range(5)}
+        return res, {k: to_host(out[k].parts[rank].buf).numpy() if k != s else None for k in range(5)}
 
     lw = LoopbackWorld(4, timeout=300)
     results = lw.run(fn)
