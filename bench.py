@@ -138,25 +138,94 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# -- the CPU reference arm (oracle port) --------------------------------------
+# -- the CPU reference arm ----------------------------------------------------
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def cpu_reference(workload: str, budget_s: float = 12.0) -> dict:
-    """Time the oracle port of the reference algorithm (numpy/OpenBLAS, every
-    host thread) on a bounded sample of the workload: the same order, modes
-    and element type, a thinner first mode.  Returns GB/s and the sample."""
+def _ref_package():
+    """The reference package ``tenvec`` as installed (unmodified) under
+    baseline/_ref, or $TENVEC_REF; None when absent."""
+    path = os.environ.get("TENVEC_REF") or REF_DIR
+    if not os.path.isdir(os.path.join(path, "tenvec")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import tenvec
+        from tenvec import bench as tb
+    except Exception:  # noqa: BLE001
+        return None
+    return tenvec, tb
+
+
+def _sample_shape(wl: dict, target_bytes: float, itemsize: int) -> tuple:
+    """The workload with its first mode thinned to ~target_bytes (the whole
+    tensor when it is smaller)."""
+    shape = list(wl["shape"])
+    per = math.prod(shape[1:]) * itemsize
+    shape[0] = max(1, min(shape[0], int(target_bytes // per)))
+    if wl["kind"] == "hopm" and wl["s"] == 0:
+        shape[0] = max(shape[0], 2)
+    return tuple(shape)
+
+
+def _cpu_threads() -> int:
+    import numpy  # noqa: F401 - load BLAS so its thread pool is visible
+
+    try:  # torchrun sets OMP_NUM_THREADS=1; the reference arm uses every host core
+        from threadpoolctl import threadpool_info, threadpool_limits
+        threadpool_limits(limits=os.cpu_count())
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def cpu_reference(wl: dict, budget_s: float = 12.0) -> dict:
+    """Time the reference's own CPU path on a bounded sample of the workload
+    (the same order, modes, split and element type, a thinner first mode):
+    the installed reference package's ``run_bench`` (tvc per mode for a
+    sweep, hopm for dHOPM3; tenvec/bench.py:280-312) when baseline/_ref holds
+    it, else the oracle port (oracle/tenvec_oracle.py).  GB/s = the
+    reference's own streamed-element count x storage bytes / time."""
+    cores = _cpu_threads()
+    ref = _ref_package()
+    if ref is not None:
+        tenvec, tb = ref
+        mode = tenvec.precision.MODES[wl["mode"]]
+        shape = _sample_shape(wl, 2e9 if wl["kind"] != "hopm" else 1e9, mode.storage_bytes)
+        dims = tenvec.Shape(shape)
+        d = len(shape)
+        if wl["kind"] == "hopm":
+            cfgs = [tb.BenchConfig("hopm", dims, s=wl["s"], workers=1, precision=mode, seconds=budget_s,
+                                   fill="integer-random", seed=1)]
+        else:
+            cfgs = [tb.BenchConfig("tvc", dims, k=k, precision=mode, seconds=budget_s / d,
+                                   fill="integer-random", seed=1) for k in range(d)]
+        nbytes, secs, iters = 0.0, 0.0, 0
+        for cfg in cfgs:
+            r = tb.run_bench(cfg)
+            nbytes += r.touched_meas * mode.storage_bytes * r.iterations
+            secs += r.elapsed_s
+            iters += r.iterations
+        what = "dHOPM3 sweep (run_bench hopm, workers=1)" if wl["kind"] == "hopm" else \
+            f"tvc k=0..{d - 1} (run_bench tvc, one config per mode)"
+        return {"value": nbytes / secs / 1e9, "unit": "GB/s", "cores": cores, "kind": "reference",
+                "sample": f"{'x'.join(map(str, shape))} {wl['mode']} {what}, {iters} timed iterations "
+                          f"in {secs:.1f} s (reference tenvec from baseline/_ref, numpy/BLAS threads)",
+                "ms_per_step": secs / max(1, iters // len(cfgs)) * 1e3}
+    return cpu_port(wl, budget_s, cores)
+
+
+def cpu_port(wl: dict, budget_s: float, cores: int) -> dict:
+    """Fallback: the oracle port of the reference algorithm (numpy/OpenBLAS)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
     import tenvec_oracle as O
 
-    wl = WORKLOADS[workload]
-    shape = list(wl["shape"])
     mode = wl["mode"]
     st = O.MODES[mode][0]
-    # the sample: shrink mode 0 so the tensor is ~0.5 GB (whole job for C1)
-    per = math.prod(shape[1:]) * st.itemsize
-    shape[0] = max(1, min(shape[0], int(5e8 // per)))
-    shape = tuple(shape)
+    shape = _sample_shape(wl, 5e8, st.itemsize)
     vals = O.demote(O.fill_values(shape, "hash", seed=1), mode).copy()
     d = len(shape)
     xs = [O.demote((np.arange(n) % 7) + 1.0, mode).copy() for n in shape]
@@ -164,22 +233,15 @@ def cpu_reference(workload: str, budget_s: float = 12.0) -> dict:
     step_bytes = sum((n_el + shape[k] + n_el // shape[k]) * st.itemsize for k in range(d))
     if wl["kind"] == "hopm":
         x0 = O.initial_vectors(shape, mode)
-        sim_bytes = None
 
         def once():
             O.dhopm3(vals.reshape(shape), wl["s"], 1, x0, 1, mode)
         import paper_2501_03121_b200.schedule as S
         step_bytes = S.sweep_bytes(shape, wl["s"], 1, st.itemsize)[0]
-        del sim_bytes
     else:
         def once():
             for k in range(d):
                 O.tvc(vals, shape, xs[k], k, mode)
-    try:  # torchrun sets OMP_NUM_THREADS=1; the reference arm uses every host core
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(limits=os.cpu_count())
-    except Exception:  # noqa: BLE001
-        pass
     once()  # warm-up
     times = []
     t_end = time.perf_counter() + budget_s
@@ -189,21 +251,12 @@ def cpu_reference(workload: str, budget_s: float = 12.0) -> dict:
         times.append(time.perf_counter() - t0)
         if len(times) >= 50:
             break
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:  # noqa: BLE001
-        cores = os.cpu_count() or 1
     avg = statistics.fmean(times)
-    return {
-        "value": step_bytes / avg / 1e9,
-        "unit": "GB/s",
-        "cores": cores,
-        "kind": "port",
-        "sample": f"{'x'.join(map(str, shape))} {mode} {'dHOPM3 sweep' if wl['kind'] == 'hopm' else 'mode sweep k=0..' + str(d - 1)}, "
-                  f"{len(times)} timed steps of {avg * 1e3:.1f} ms (oracle/tenvec_oracle.py, numpy/OpenBLAS)",
-        "ms_per_step": avg * 1e3,
-    }
+    what = "dHOPM3 sweep" if wl["kind"] == "hopm" else f"mode sweep k=0..{d - 1}"
+    return {"value": step_bytes / avg / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{'x'.join(map(str, shape))} {mode} {what}, {len(times)} timed steps of "
+                      f"{avg * 1e3:.1f} ms (oracle/tenvec_oracle.py: baseline/_ref not installed)",
+            "ms_per_step": avg * 1e3}
 
 
 # -- our arm ------------------------------------------------------------------
@@ -226,9 +279,9 @@ def _setup_dist(n_gpus: int):
 
 
 def run_ours(args) -> dict | None:
-    import numpy as np
+    import gc
+
     import torch
-    import torch.distributed as dist
 
     import paper_2501_03121_b200 as tv
     from paper_2501_03121_b200 import build
@@ -236,6 +289,27 @@ def run_ours(args) -> dict | None:
     build.build()
     world, rank, local = _setup_dist(args.gpus)
     wl = WORKLOADS[args.workload]
+    if wl["kind"] == "hopm":
+        return run_hopm(args, tv, wl, world, rank)
+    line = run_sweep(args, tv, wl, world, rank)
+    hw = args.hopm_workload
+    if hw == "auto":
+        hw = "c4" if args.workload == "c2" and not args.shape else "none"
+    if hw != "none":
+        # the dHOPM3 half of the metric, on a fresh tensor (the sweep's is freed)
+        gc.collect()
+        torch.cuda.empty_cache()
+        hline = run_hopm(args, tv, WORKLOADS[hw], world, rank)
+        if line is not None:
+            line["hopm"] = hline
+    return line
+
+
+def run_sweep(args, tv, wl, world, rank) -> dict | None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
     mode = tv.MODES[wl["mode"]]
     shape = tv.Shape(wl["shape"])
     s = wl["s"]
@@ -248,9 +322,6 @@ def run_ours(args) -> dict | None:
     sb = mode.storage_bytes
     xs = [torch.from_numpy(tv_demote_host(np.arange(n) % 7 + 1.0, mode)).cuda() for n in shape.extents]
     torch.cuda.synchronize()
-
-    if wl["kind"] == "hopm":
-        return run_hopm(args, tv, dt, world, rank, wl, mode, group)
 
     # per-mode algorithmic bytes of this rank (kernel traffic) and collective bytes
     mode_bytes, comm_bytes, regimes = [], 0, []
@@ -289,16 +360,19 @@ def run_ours(args) -> dict | None:
     if clocks:
         clocks.start()
     torch.cuda.synchronize()
+    last = None
     for i in range(args.steps):
         if flush is not None:
             flush()
         ev[i][0].record()
-        step()
+        last = step()
         ev[i][1].record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
+    parity = check_sweep(tv, dt, last, xs, wl, world, me)
+    del last
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
@@ -381,13 +455,62 @@ def run_ours(args) -> dict | None:
         "dominant_frac_of_read_stream": round(achieved / read_gbs, 4),
         "comm_bytes_per_step_per_gpu": comm_bytes,
         "e2e": e2e,
+        "parity": parity,
         "gpu_launches": args.steps * (d + (1 if world > 1 else 0)),
         "step_overlap": "split-mode reduction on a side stream under the other modes" if world > 1 else None,
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = {k: v for k, v in cpu_reference(args.workload).items() if k != "ms_per_step"}
+        line["cpu_baseline"] = {k: v for k, v in cpu_reference(wl).items() if k != "ms_per_step"}
     return line
+
+
+def _all_ok(ok: bool, world: int) -> bool:
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return ok
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
+def check_sweep(tv, dt, res, xs, wl, world, me, samples: int = 64) -> dict:
+    """Sampled outputs of the LAST timed step, bitwise against the closed
+    form of the hash fill (paper_2501_03121_b200/verify.py): every rank checks
+    the outputs it holds -- its own slab's contraction for k != s, the
+    replicated reduced result for k == s -- and the verdict is the AND over
+    ranks."""
+    import numpy as np
+    import torch
+
+    from paper_2501_03121_b200 import verify
+
+    shape = tuple(wl["shape"])
+    s = wl["s"]
+    mode = dt.mode
+    a, b = dt.plan.ranges[me]
+    ok, checked = True, 0
+    for k, out in sorted(res.items()):
+        buf = next(p for p in out.parts if p is not None).buf
+        x = xs[k].double().cpu().numpy() if mode.storage != "brain" else \
+            (xs[k].cpu().numpy().astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        if k == s:
+            idx = verify.sample_outputs(shape, k, samples, seed=k)
+            want = verify.tvc_expected(shape, k, x, "hash", 1, idx)
+        else:
+            loc = list(shape)
+            loc[s] = b - a
+            idx = verify.sample_outputs(loc, k, samples, seed=k)
+            want = verify.tvc_expected_slab(shape, s, a, b, k, x, "hash", 1, idx)
+        got = buf[torch.from_numpy(idx).to(buf.device)].cpu().numpy()
+        ok &= verify.check_tvc_samples(got, want, mode.storage)
+        checked += idx.size
+    ok = _all_ok(ok, world)
+    return {"status": "ok" if ok else "FAILED", "outputs_checked_per_rank": checked,
+            "how": "last timed step: sampled outputs of every mode bitwise vs the closed form of the "
+                   "hash fill (exact integer sums), on every rank"}
 
 
 def _block_stream(torch, cycles: int = 2_000_000) -> None:
@@ -532,15 +655,30 @@ def run_e2e_sweep(args, tv, dt, part, xs, s, world, rank, group, job_bytes_step)
     return out
 
 
-def run_hopm(args, tv, dt, world, rank, wl, mode, group):
+def run_hopm(args, tv, wl, world, rank) -> dict | None:
+    """One dHOPM3 run of ``args.steps`` sweeps through the public ``dhopm3``
+    on a device-generated tensor split along wl["s"] over the N GPUs.
+
+    value = schedule.sweep_bytes (the reference cost model's streamed bytes
+    of a sweep, summed over ranks) x sweeps / event-timed device time of the
+    call; e2e = the same bytes / wall time of a second identical call (start
+    vectors from the host, final vectors and norms back to the host -- what
+    the call returns); parity = the last update of the timed run (x_{d-1}
+    and lambda) against the closed form of the fill at sampled indices."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    shape = dt.global_shape()
+    from paper_2501_03121_b200 import verify
+
+    mode = tv.MODES[wl["mode"]]
+    shape = tv.Shape(wl["shape"])
+    s = wl["s"]
+    group = tv.RankGroup() if world > 1 else None
+    dt = tv.distribute_generated(shape, s, world, mode, fill="hash", seed=1, group=group)
     x0 = tv.initial_vectors(shape, mode)
     sweeps = args.steps
-    tv.dhopm3(dt, x0, sweeps=max(1, args.warmup))
+    tv.dhopm3(dt, x0, sweeps=max(3, args.warmup))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -558,10 +696,25 @@ def run_hopm(args, tv, dt, world, rank, wl, mode, group):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    per_rank = tv.schedule.sweep_bytes(shape.extents, wl["s"], world, mode.storage_bytes)
+    per_rank = tv.schedule.sweep_bytes(shape.extents, s, world, mode.storage_bytes)
     job = sum(per_rank)
     value = job * sweeps / (ms / 1e3) / 1e9
     peak = float(_peaks().get("hbm_gbs", 6650.0))
+
+    # e2e: the same call by wall clock (host vectors in, host vectors out)
+    if world > 1:
+        dist.barrier()
+    w0 = time.perf_counter()
+    res2 = tv.dhopm3(dt, x0, sweeps=sweeps)
+    wall = time.perf_counter() - w0
+    t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    wall = float(t.item())
+    h2d = sum(np.asarray(v).nbytes for v in x0)
+    d2h = sum(np.asarray(v).nbytes for v in res2.vectors) + 8 * sum(len(n) for n in res2.norms)
+    same = res2.norms == res.norms and all(np.array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
+                                          for a, b in zip(res.vectors, res2.vectors))
 
     # roofline: the two full-slab contractions that carry ~99 % of a sweep's
     # bytes (the first TVC of iterations j = 0 and j = 1), each timed alone on
@@ -588,16 +741,28 @@ def run_hopm(args, tv, dt, world, rank, wl, mode, group):
                      "gbs": round(nbytes / kms / 1e6, 1), "bytes": nbytes})
         del outk
     dom = max(kern, key=lambda e: e["ms"])
+    del dt, part
     if rank != 0:
         return None
-    return {
+
+    # parity of the timed run: x_{d-1} * lambda == A x_0 ... x_{d-2} at samples
+    n_last = shape.extents[-1]
+    idx = np.unique(np.array([0, n_last // 3, n_last - 1]))
+    vecs = [tv.promote(v, mode).astype(np.float64) for v in res.vectors]
+    lam = res.norms[-1][-1]
+    want = verify.hopm_last_update_expected(shape.extents, vecs[:-1], "hash", 1, idx) / lam
+    tol = {"f64": 1e-12, "f32": 1e-5, "f32f64": 1e-6, "f16f32": 2e-3, "bf16f32": 1.6e-2}[mode.name]
+    rel = float(np.max(np.abs(vecs[-1][idx] - want) / np.abs(want)))
+    ok = rel <= tol and same
+    line = {
         "metric": "dHOPM3 achieved HBM GB/s (aggregate over GPUs)",
         "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": sweeps,
-        "warmup": args.warmup, "ms_per_step": round(ms / sweeps, 4), "higher_is_better": True,
+        "warmup": max(3, args.warmup), "ms_per_step": round(ms / sweeps, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": mode.name,
         "data": "synthetic (hash fill in [1,97] generated on device)",
         "config": {"workload": wl["desc"], "shape": list(shape.extents), "precision": mode.name,
-                   "split_mode": wl["s"], "p": world, "parallelism": f"split{world}"},
+                   "split_mode": s, "p": world, "parallelism": f"split{world}",
+                   "l2": "tensor >> 126 MB L2, no flush", "step": "one dHOPM3 sweep (d updates)"},
         "per_gpu_gbs": round(value / world, 2),
         "roofline_frac_aggregate": round(value / (peak * world), 4),
         "roofline": {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
@@ -605,10 +770,22 @@ def run_hopm(args, tv, dt, world, rank, wl, mode, group):
                      "kernel": f"tv_tvc k={dom['k']} ({dom['regime']}) on the rank's full slab",
                      "bytes_per_launch": dom["bytes"]},
         "full_slab_passes": kern,
+        "e2e": {"value": round(job * sweeps / wall / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d // sweeps,
+                "d2h_bytes_per_step": d2h // sweeps, "ms_per_step": round(wall * 1e3 / sweeps, 4),
+                "path": f"public dhopm3 call of {sweeps} sweeps by wall clock: start vectors from host "
+                        "memory, final vectors + norms back to host (bytes per step = per call / sweeps)"},
+        "parity": {"status": "ok" if ok else "FAILED", "max_rel_err": rel, "tol": tol,
+                   "repeat_bitwise": same,
+                   "how": "timed run's last update: x_{d-1}[i] * lambda vs the fill's closed form "
+                          "sum A[..., i] prod x_m at 3 sampled i (float64 on the host); e2e rerun "
+                          "bit-identical"},
         "tvc_launches": res.tvc_count,
-        "lambda_last": res.norms[-1][-1],
+        "lambda_last": lam,
         "clocks": clk,
     }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = {k: v for k, v in cpu_reference(wl).items() if k != "ms_per_step"}
+    return line
 
 
 def main(argv=None) -> int:
@@ -623,6 +800,8 @@ def main(argv=None) -> int:
     ap.add_argument("--graph", type=int, default=None,
                     help="1: time the sweep as a captured CUDA graph (tv.SweepGraph; one GPU only); "
                          "default: on for launch-bound workloads (c1)")
+    ap.add_argument("--hopm-workload", default="auto", choices=["auto", "none", "c4", "c5"],
+                    help="dHOPM3 leg after the sweep (auto: c4 after the default c2 run)")
     ap.add_argument("--shape", default=None, help="override the workload shape, e.g. 1024,1024,1024 (profiling)")
     args = ap.parse_args(argv)
     if args.shape:
@@ -638,7 +817,8 @@ def main(argv=None) -> int:
         if rank != 0:
             return 0
         wl = WORKLOADS[args.workload]
-        cb = cpu_reference(args.workload, budget_s=max(5.0, min(60.0, 2.0 * args.steps)))
+        budget = max(5.0, min(60.0, 2.0 * args.steps))
+        cb = cpu_reference(wl, budget_s=budget)
         line = {
             "impl": "reference",
             "metric": "dTVC achieved HBM GB/s (aggregate over GPUs)" if wl["kind"] != "hopm"
@@ -653,6 +833,19 @@ def main(argv=None) -> int:
             "e2e": {"value": round(cb["value"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
+        hw = args.hopm_workload
+        if hw == "auto":
+            hw = "c4" if args.workload == "c2" and not args.shape else "none"
+        if hw != "none":
+            hwl = WORKLOADS[hw]
+            hb = cpu_reference(hwl, budget_s=budget)
+            line["hopm"] = {"metric": "dHOPM3 achieved HBM GB/s (aggregate over GPUs)",
+                            "value": round(hb["value"], 3), "unit": "GB/s", "dtype": hwl["mode"],
+                            "config": {"workload": hwl["desc"], "shape": list(hwl["shape"]),
+                                       "precision": hwl["mode"], "split_mode": hwl["s"], "p": args.gpus},
+                            "cpu_baseline": {k: v for k, v in hb.items() if k != "ms_per_step"},
+                            "e2e": {"value": round(hb["value"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                    "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
 

@@ -19,7 +19,8 @@ import math
 
 import numpy as np
 
-__all__ = ["fill_at", "tvc_expected", "sample_outputs", "check_tvc_samples"]
+__all__ = ["fill_at", "tvc_expected", "tvc_expected_slab", "sample_outputs", "check_tvc_samples",
+           "hopm_last_update_expected"]
 
 _MASK = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -67,6 +68,46 @@ def tvc_expected(extents, k: int, x: np.ndarray, kind: str, seed: int, out_idx: 
     g = (i[:, None] * nk + j[None, :]) * v + r[:, None]
     vals = fill_at(kind, seed, g.astype(np.uint64))
     return vals @ np.asarray(x, dtype=np.float64)
+
+
+def tvc_expected_slab(extents, s: int, lo: int, hi: int, k: int, x: np.ndarray, kind: str, seed: int,
+                      out_idx: np.ndarray) -> np.ndarray:
+    """tvc_expected for the rank-local slab [lo, hi) along mode s of the
+    filled global tensor (k != s: the rank's own output; out_idx indexes the
+    contraction of the slab)."""
+    ext = [int(e) for e in extents]
+    loc = list(ext)
+    loc[s] = hi - lo
+    nk = loc[k]
+    v = math.prod(loc[k + 1:])
+    out_idx = np.asarray(out_idx, dtype=np.int64)
+    i, r = np.divmod(out_idx, v)
+    j = np.arange(nk, dtype=np.int64)
+    flat = (i[:, None] * nk + j[None, :]) * v + r[:, None]  # local linear index
+    multi = list(np.unravel_index(flat, loc))
+    multi[s] = multi[s] + lo
+    g = np.ravel_multi_index(multi, ext).astype(np.uint64)
+    return fill_at(kind, seed, g) @ np.asarray(x, dtype=np.float64)
+
+
+def hopm_last_update_expected(extents, vectors, kind: str, seed: int, idx: np.ndarray) -> np.ndarray:
+    """The last update of a dHOPM3 sweep contracts every mode but the last
+    with the sweep's final vectors x_0 .. x_{d-2}: y[i] = sum A[..., i]
+    prod x_m.  Returns y at the sampled last-mode indices in float64 (one
+    (n_0 ... n_{d-2}) slice of the fill per sample); the run's x_{d-1}[i]
+    must equal y[i] / lambda, lambda = ||y|| = the sweep's last norm."""
+    ext = [int(e) for e in extents]
+    d = len(ext)
+    n_last = ext[-1]
+    lead = math.prod(ext[:-1])
+    base = np.arange(lead, dtype=np.uint64) * np.uint64(n_last)
+    out = []
+    for i in np.asarray(idx, dtype=np.int64):
+        a = fill_at(kind, seed, base + np.uint64(i)).reshape(ext[:-1])
+        for m in range(d - 2, -1, -1):  # contract the trailing mode first
+            a = a @ np.asarray(vectors[m], dtype=np.float64)
+        out.append(float(a))
+    return np.asarray(out)
 
 
 def check_tvc_samples(got: np.ndarray, expected: np.ndarray, storage: str) -> bool:
