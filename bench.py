@@ -451,6 +451,11 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
                      if not peaks.get("_fallback") else "fallback 6650 GB/s"},
         "modes": modes,
+        "roofline_sweep": None if world > 1 else {
+            "achieved": round(value, 1), "peak": peak, "unit": "GB/s", "frac": round(value / peak, 4),
+            "kernel": f"tv_tvc_sweep: the {d} mode grids of a step issued by one C call, each mode after "
+                      "the first launched with programmatic dependent launch (its ramp overlaps the "
+                      "previous mode's tail); per-step bytes / per-step event time"},
         "read_stream_gbs": round(read_gbs, 1),
         "dominant_frac_of_read_stream": round(achieved / read_gbs, 4),
         "comm_bytes_per_step_per_gpu": comm_bytes,

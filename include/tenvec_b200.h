@@ -15,6 +15,7 @@
  * There is no CPU fallback: a missing or failing device raises TV_ECUDA.
  *
  * Reference interfaces replaced (paths relative to the reference pkg/src/tenvec):
+ *   tv_tvc_sweep    bench.py:209-215    the per-mode tvc loop of a dTVC mode sweep
  *   tv_tvc, tv_tvc_ws kernels.py:126-171 tvc_native (and getvc, kernels.py:73-123,
  *                                       through the (u, n_k, v) block view)
  *   tv_getvc(_ws)   kernels.py:73-123   getvc over a strided m x n view (lda >= n)
@@ -93,6 +94,17 @@ int64_t tv_tvc_workspace_bytes(const void* A, int storage, int compute, int64_t 
 int tv_tvc_ws(const void* A, int storage, int compute, int64_t u, int64_t nk, int64_t v,
               const void* x, double alpha, double beta, void* y, void* ws, int64_t ws_bytes,
               void* stream);
+
+/* The mode sweep (the unit of the paper's dTVC benchmarks, bench.py:209-215):
+ * ys[k] <- A x_k xs[k] for every mode k = 0..d-1 of the contiguous order-d
+ * tensor A (extents ext[0..d-1], last fastest), alpha = 1, beta = 0 -- each
+ * output bit-identical to tv_tvc_ws on that mode's (u, n_k, v) view.  Modes
+ * after the first launch with programmatic stream serialization: outputs
+ * must be distinct and must not alias A.  ws: at least
+ * tv_tvc_sweep_workspace_bytes (NULL when that is 0); allocates nothing. */
+int tv_tvc_sweep(const void* A, int storage, int compute, int d, const int64_t* ext, const void* const* xs,
+                 void* const* ys, void* ws, int64_t ws_bytes, void* stream);
+int64_t tv_tvc_sweep_workspace_bytes(const void* A, int storage, int compute, int d, const int64_t* ext);
 
 /* The same contraction through the naive scalar kernel only (one thread per
  * output for v > 1, one warp per row for v == 1): the "looped" cross-check of

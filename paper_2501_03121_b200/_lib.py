@@ -43,6 +43,9 @@ SIGNATURES = {
     "tv_getvc_ws": (_int, [_int, _vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double,
                            _vp, _vp, _i64, _vp]),
     "tv_getvc_workspace_bytes": (_i64, [_int, _vp, _int, _int, _i64, _i64, _i64]),
+    "tv_tvc_sweep": (_int, [_vp, _int, _int, _int, ctypes.POINTER(_i64), ctypes.POINTER(_vp),
+                            ctypes.POINTER(_vp), _vp, _i64, _vp]),
+    "tv_tvc_sweep_workspace_bytes": (_i64, [_vp, _int, _int, _int, ctypes.POINTER(_i64)]),
     "tv_tvc_naive": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, ctypes.c_double, ctypes.c_double, _vp, _vp]),
     "tv_tvc_normalize": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tv_tvc_regime": (_int, [_vp, _int, _i64, _i64, _i64]),

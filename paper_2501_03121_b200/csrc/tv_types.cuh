@@ -87,6 +87,17 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 
 // 16-byte streaming load: read-only path, no L1 allocation, 256B L2 prefetch.
+// Programmatic dependent launch (tv_tvc_sweep): every TVC kernel lets the
+// next grid of the stream launch as soon as all of its CTAs are resident
+// (griddepcontrol.launch_dependents at entry) and, before exiting, waits for
+// the grids it was launched after (griddepcontrol.wait) -- so a PDL-launched
+// mode overlaps the previous mode's tail but still completes after it, and
+// stream order holds for whatever follows.  Both are no-ops in a plain launch.
+struct PdlScope {
+  __device__ __forceinline__ PdlScope() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+  __device__ __forceinline__ ~PdlScope() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+};
+
 __device__ __forceinline__ uint4 ld_stream16(const void* p) {
   uint4 r;
   asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"

@@ -59,6 +59,32 @@ namespace tv {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
+// Launches of the TVC kernels.  Inside tv_tvc_sweep every mode after the
+// first is launched with programmatic stream serialization (the modes are
+// independent: same read-only tensor, distinct outputs), so its CTAs fill
+// the SMs the previous mode's tail frees; PdlScope keeps completion order.
+static thread_local bool t_pdl = false;
+
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args... args) {
+  if (!t_pdl) {
+    kern<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // a lane's load: one 16-byte vector (AL) or one element
 template <int SD, typename C, bool AL>
 struct Unit {
@@ -92,6 +118,7 @@ __global__ void __launch_bounds__(kThreads)
     k_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
            typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t su, C alpha, C beta,
            int has_beta) {
+  PdlScope pdl_scope;
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
   constexpr int QPL = QB / RS;  // loads per lane per row in one batch
@@ -238,6 +265,7 @@ __global__ void __launch_bounds__(kThreads)
     k_rows_short(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
                  typename St<SD>::T* __restrict__ y, int64_t u, int nk, int64_t su, C alpha,
                  C beta, int has_beta) {
+  PdlScope pdl_scope;
   constexpr int VEC = VecN<SD>::N;
   __shared__ C xs[8 * VEC];
   const int nkv = nk / VEC;
@@ -288,6 +316,7 @@ __global__ void __launch_bounds__(kThreads)
            typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk_all, int64_t v, int64_t su,
            int64_t sk, int64_t ntile, C alpha, C beta, int has_beta, int64_t rpc,
            C* __restrict__ ws) {
+  PdlScope pdl_scope;
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
   constexpr int CW = kWarps / JR;
@@ -448,6 +477,7 @@ __global__ void __launch_bounds__(kThreads)
     k_flat(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
            typename St<SD>::T* __restrict__ y, int64_t u, int nk, int v, C alpha, C beta,
            int has_beta) {
+  PdlScope pdl_scope;
   constexpr int VEC = VecN<SD>::N;
   constexpr int B = P * K;  // steps per batch (a multiple of P: slots are compile-time)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -539,6 +569,7 @@ __global__ void __launch_bounds__(kThreads)
     k_flat_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
                 typename St<SD>::T* __restrict__ y, int64_t u, int nk, C alpha, C beta,
                 int has_beta) {
+  PdlScope pdl_scope;
   constexpr int VEC = VecN<SD>::N;
   __shared__ C xs[32 * 8];  // nk <= 32 vectors of <= 8 elements
   __shared__ C part[kWarps][K][32 * S];
@@ -598,6 +629,7 @@ __global__ void __launch_bounds__(kThreads)
             typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int v, int64_t su,
             int64_t sk, C alpha, C beta, int has_beta, int64_t nch, int64_t rpc,
             C* __restrict__ ws) {
+  PdlScope pdl_scope;
   using U = Unit<SD, C, AL>;
   constexpr int N = U::N;
   __shared__ C red[kWarps][32][N + (sizeof(C) == 8 ? 0 : 1)];
@@ -732,6 +764,7 @@ __global__ void __launch_bounds__(kThreads)
     k_staged(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
              typename St<SD>::T* __restrict__ y, int64_t u, int nk, int v, int spt, int64_t ntiles,
              int G, int sbytes, int nst, C alpha, C beta, int has_beta) {
+  PdlScope pdl_scope;
   using T = typename St<SD>::T;
   constexpr int SB = sizeof(T);
   constexpr int VEC = VecN<SD>::N;
@@ -885,6 +918,7 @@ __global__ void __launch_bounds__(kThreads)
     k_staged_long(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
                   typename St<SD>::T* __restrict__ y, int64_t u, int nk, int v, int tps, int G,
                   int sbytes, C alpha, C beta, int has_beta) {
+  PdlScope pdl_scope;
   using T = typename St<SD>::T;
   constexpr int SB = sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1021,6 +1055,7 @@ __global__ void __launch_bounds__(kNormThreads)
     k_tvc_norm(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
                typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t v, int64_t ncb,
                double* __restrict__ norm_out, int32_t* __restrict__ status, unsigned* counter) {
+  PdlScope pdl_scope;
   using T = typename St<SD>::T;
   constexpr int VEC = VecN<SD>::N;
   constexpr int NW = kNormThreads / 32;
@@ -1087,6 +1122,7 @@ __global__ void __launch_bounds__(kThreads)
     k_naive_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
                  typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t su, int64_t sk,
                  C alpha, C beta, int has_beta) {
+  PdlScope pdl_scope;
   const int lane = threadIdx.x & 31;
   const int64_t warps_total = (int64_t)gridDim.x * kWarps;
   for (int64_t i = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); i < u; i += warps_total) {
@@ -1104,6 +1140,7 @@ __global__ void __launch_bounds__(kThreads)
     k_naive_cols(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
                  typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t v, int64_t su,
                  int64_t sk, C alpha, C beta, int has_beta) {
+  PdlScope pdl_scope;
   const int64_t total = u * v;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
        o += (int64_t)gridDim.x * blockDim.x) {
@@ -1173,7 +1210,15 @@ static int pick_col_phases(int64_t nk, int64_t stripes, int64_t u, int sb = 0) {
   int cw_max = 1;
   while (cw_max < kWarps && cw_max * 2 <= stripes) cw_max *= 2;
   if (kWarps / jr > cw_max) jr = kWarps / cw_max;
-  const int64_t want = 4LL * sm_count();
+  static const int want_env = [] {  // TENVEC_B200_COL_WANT: target CTAs per SM, for A/B runs
+    const char* e = getenv("TENVEC_B200_COL_WANT");
+    return e ? atoi(e) : 0;
+  }();
+  // at least one CTA per SM; more row phases only when the column blocks
+  // cannot cover the SMs (C1 256^3 k = 0/1: 256 blocks of 2 phases stream at
+  // 28.7 us vs 30.7 for 1024 blocks of 8, which need 1.7 waves at 4 per SM;
+  // larger views are unaffected -- profiles/r02_cols_want_ab/)
+  const int64_t want = (want_env > 0 ? want_env : 1) * (int64_t)sm_count();
   while (jr < kWarps && jr < nk && u * cdiv(stripes, kWarps / jr) < want) jr *= 2;
   return jr;
 }
@@ -1307,11 +1352,10 @@ static void launch_rows(const void* A, const void* x, void* y, int64_t u, int64_
     auto kern = k_rows<SD, C, G, RS, (LONG && !PEEL) ? kRowBatchLong : kRowBatch, true, PEEL, LONG>;
     if (xs_bytes > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs_bytes);
-    kern<<<grid, kThreads, xs_bytes, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
+    launch_k(kern, grid, kThreads, xs_bytes, st, (const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
   } else if constexpr (G == 32 && RS == 1 && LONG) {
     // rows longer than the shared-memory copy of x: x through L1
-    k_rows<SD, C, 32, 1, kRowBatch, false, PEEL, true>
-        <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
+    launch_k(k_rows<SD, C, 32, 1, kRowBatch, false, PEEL, true>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
   }
 }
 
@@ -1479,12 +1523,12 @@ static void launch_staged(const void* A, const void* x, void* y, int64_t u, int6
   if (vrow) {
     auto kern = k_staged<SD, C, true>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, spt,
+    launch_k(kern, grid, kThreads, smem, st, (const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, spt,
                                        ntiles, G, sbytes, nst, al, be, hb);
   } else {
     auto kern = k_staged<SD, C, false>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, spt,
+    launch_k(kern, grid, kThreads, smem, st, (const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, spt,
                                        ntiles, G, sbytes, nst, al, be, hb);
   }
 }
@@ -1509,7 +1553,7 @@ static void launch_staged_long(const void* A, const void* x, void* y, int64_t u,
   const unsigned grid = (unsigned)std::min<int64_t>(u, (int64_t)per_sm * sm_count());
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, tps, G, sbytes,
+    launch_k(kern, grid, kThreads, smem, st, (const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, tps, G, sbytes,
                                        al, be, hb);
   };
   if (M <= 1) go(k_staged_long<SD, C, 1>);
@@ -1567,7 +1611,7 @@ static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t
   // registers and measured 3-6 % faster (paper d = 4..8, profiles/r01_cols_u_ab/)
   const bool sp = nch > 1;
   auto go = [&](auto kern) {
-    kern<<<b, kThreads, 0, st>>>(At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb, rpc, ws);
+    launch_k(kern, b, kThreads, 0, st, At, xt, yt, u, nk, v, su, sk, ntile, al, be, hb, rpc, ws);
     return done();
   };
   if (!AL && VEC <= 4 && (JR == 4 || (JR == 1 && nk <= 16))) {
@@ -1628,8 +1672,7 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       const int nkv = (int)(nk / VEC);
       const int64_t rows_per_block = kWarps * (32 / nkv) * UNR;
       const unsigned grid = grid_for(u, rows_per_block, 32);
-      k_rows_short<SD, C, UNR>
-          <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, su, al, be, hb);
+      launch_k(k_rows_short<SD, C, UNR>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, (int)nk, su, al, be, hb);
       break;
     }
     case REG_COLS:
@@ -1648,10 +1691,10 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       T* yt = (T*)y;
       const int ik = (int)nk;
       switch (S) {
-        case 1: k_flat_rows<SD, C, 1, 8><<<grid_for(nblocks, kWarps * 8, 32), kThreads, 0, st>>>(At, xt, yt, u, ik, al, be, hb); break;
-        case 3: k_flat_rows<SD, C, 3, 2><<<grid_for(nblocks, kWarps * 2, 32), kThreads, 0, st>>>(At, xt, yt, u, ik, al, be, hb); break;
-        case 5: k_flat_rows<SD, C, 5, 1><<<grid_for(nblocks, kWarps, 32), kThreads, 0, st>>>(At, xt, yt, u, ik, al, be, hb); break;
-        default: k_flat_rows<SD, C, 7, 1><<<grid_for(nblocks, kWarps, 32), kThreads, 0, st>>>(At, xt, yt, u, ik, al, be, hb); break;
+        case 1: launch_k(k_flat_rows<SD, C, 1, 8>, grid_for(nblocks, kWarps * 8, 32), kThreads, 0, st, At, xt, yt, u, ik, al, be, hb); break;
+        case 3: launch_k(k_flat_rows<SD, C, 3, 2>, grid_for(nblocks, kWarps * 2, 32), kThreads, 0, st, At, xt, yt, u, ik, al, be, hb); break;
+        case 5: launch_k(k_flat_rows<SD, C, 5, 1>, grid_for(nblocks, kWarps, 32), kThreads, 0, st, At, xt, yt, u, ik, al, be, hb); break;
+        default: launch_k(k_flat_rows<SD, C, 7, 1>, grid_for(nblocks, kWarps, 32), kThreads, 0, st, At, xt, yt, u, ik, al, be, hb); break;
       }
       break;
     }
@@ -1664,7 +1707,7 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       auto go = [&](auto kern) {
         if (smem > 48 * 1024)
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, kThreads, smem, st>>>((const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, al,
+        launch_k(kern, grid, kThreads, smem, st, (const T*)A, (const T*)x, (T*)y, u, (int)nk, (int)v, al,
                                            be, hb);
       };
       if (P == 1) go(k_flat<SD, C, 1, 8>);
@@ -1680,10 +1723,10 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       const int64_t rpc = cdiv(nk, nch);
       const unsigned grid = grid_for(u * nch, kWarps, 32);
       if (reg == REG_SLABS)
-        k_slabs<SD, C, 4, true><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
+        launch_k(k_slabs<SD, C, 4, true>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
                                                            su, sk, al, be, hb, nch, rpc, ws);
       else
-        k_slabs<SD, C, 8, false><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
+        launch_k(k_slabs<SD, C, 8, false>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
                                                             su, sk, al, be, hb, nch, rpc, ws);
       if (ws != nullptr) split_finish<SD, C>(ws, wsa, nch, u, v, y, al, be, hb, st);
       break;
@@ -1691,11 +1734,10 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
     default: {
       if (v == 1) {
         const unsigned grid = grid_for(u, kWarps, 32);
-        k_naive_rows<SD, C>
-            <<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, su, sk, al, be, hb);
+        launch_k(k_naive_rows<SD, C>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, su, sk, al, be, hb);
       } else {
         const unsigned grid = grid_for(u * v, kThreads, 32);
-        k_naive_cols<SD, C><<<grid, kThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, v,
+        launch_k(k_naive_cols<SD, C>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, v,
                                                        su, sk, al, be, hb);
       }
     }
@@ -1715,10 +1757,10 @@ static int tvc_norm_typed(const void* A, int64_t u, int64_t nk, int64_t v, const
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(work, 2LL * sm_count()));
   const bool al = v == 1 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && nk % VEC == 0;
   if (al)
-    k_tvc_norm<SD, C, true><<<grid, kNormThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, v, ncb,
+    launch_k(k_tvc_norm<SD, C, true>, grid, kNormThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, v, ncb,
                                                            norm_out, status, counter);
   else
-    k_tvc_norm<SD, C, false><<<grid, kNormThreads, 0, st>>>((const T*)A, (const T*)x, (T*)y, u, nk, v, ncb,
+    launch_k(k_tvc_norm<SD, C, false>, grid, kNormThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, v, ncb,
                                                             norm_out, status, counter);
   return check_launch("tv_tvc_normalize");
 }
@@ -1779,6 +1821,77 @@ extern "C" int tv_tvc_ws(const void* A, int storage, int compute, int64_t u, int
     return tv::set_error(TV_EKERNEL, "tv_tvc: null pointer");
   return tv::tvc_dispatch(A, storage, compute, u, nk, v, nk * v, v, x, alpha, beta, y, stream, 0,
                           ws, ws_bytes, 1);
+}
+
+// ---------------------------------------------------------------- sweep ----
+// The mode sweep of the paper's dTVC benchmarks: y_k = A x_k x_k for every
+// mode k of one order-d tensor, independent outputs.  One regime launch per
+// mode (exactly tv_tvc_ws's, so every y_k has tv_tvc's bits); modes after the
+// first launch with programmatic stream serialization so a mode's ramp
+// overlaps the previous mode's tail on small tensors.  Each mode's split-K
+// workspace gets its own 256-byte-aligned slice (modes may overlap).
+namespace {
+struct SweepView {
+  int64_t u, nk, v;
+};
+
+int sweep_views(int d, const int64_t* ext, SweepView* out) {
+  if (d < 1 || d > 64 || ext == nullptr) return tv::set_error(TV_EKERNEL, "tv_tvc_sweep: need 1 <= d <= 64");
+  for (int k = 0; k < d; ++k)
+    if (ext[k] < 1) return tv::set_error(TV_EKERNEL, "tv_tvc_sweep: extents must be >= 1");
+  for (int k = 0; k < d; ++k) {
+    int64_t u = 1, v = 1;
+    for (int i = 0; i < k; ++i) u *= ext[i];
+    for (int i = k + 1; i < d; ++i) v *= ext[i];
+    out[k] = {u, ext[k], v};
+  }
+  return TV_OK;
+}
+
+int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+}  // namespace
+
+extern "C" int64_t tv_tvc_sweep_workspace_bytes(const void* A, int storage, int compute, int d,
+                                                const int64_t* ext) {
+  SweepView vw[64];
+  if (sweep_views(d, ext, vw) != TV_OK) return -1;
+  int64_t total = 0;
+  for (int k = 0; k < d; ++k) {
+    const int64_t b = tv::ws_bytes_dispatch(A, storage, compute, vw[k].u, vw[k].nk, vw[k].v,
+                                            vw[k].nk * vw[k].v, vw[k].v);
+    if (b < 0) return -1;
+    total += align256(b);
+  }
+  return total;
+}
+
+extern "C" int tv_tvc_sweep(const void* A, int storage, int compute, int d, const int64_t* ext,
+                            const void* const* xs, void* const* ys, void* ws, int64_t ws_bytes, void* stream) {
+  SweepView vw[64];
+  int rc = sweep_views(d, ext, vw);
+  if (rc != TV_OK) return rc;
+  if (A == nullptr || xs == nullptr || ys == nullptr) return tv::set_error(TV_EKERNEL, "tv_tvc_sweep: null pointer");
+  char* wp = static_cast<char*>(ws);
+  int64_t left = ws_bytes;
+  for (int k = 0; k < d && rc == TV_OK; ++k) {
+    if (xs[k] == nullptr || ys[k] == nullptr) {
+      rc = tv::set_error(TV_EKERNEL, "tv_tvc_sweep: null vector or output");
+      break;
+    }
+    const SweepView& w = vw[k];
+    const int64_t need = align256(tv::ws_bytes_dispatch(A, storage, compute, w.u, w.nk, w.v, w.nk * w.v, w.v));
+    if (need > left) {
+      rc = tv::set_error(TV_EKERNEL, "tv_tvc_sweep: workspace smaller than tv_tvc_sweep_workspace_bytes");
+      break;
+    }
+    tv::t_pdl = k > 0;
+    rc = tv::tvc_dispatch(A, storage, compute, w.u, w.nk, w.v, w.nk * w.v, w.v, xs[k], 1.0, 0.0, ys[k], stream, 0,
+                          need ? wp : nullptr, need, 1);
+    wp += need;
+    left -= need;
+  }
+  tv::t_pdl = false;
+  return rc;
 }
 
 extern "C" int64_t tv_tvc_workspace_bytes(const void* A, int storage, int compute, int64_t u, int64_t nk,

@@ -121,6 +121,26 @@ def launch_getvc(trans: int, a_ptr: int, mode: PrecisionMode, m: int, n: int, ld
     del keep
 
 
+def launch_sweep(t, xvs: list, ys: list, stream: torch.cuda.Stream | None = None) -> None:
+    """tv_tvc_sweep: ys[k] <- t x_k xvs[k] for every mode k of the contiguous
+    device tensor t (device vectors in the storage format, preallocated
+    outputs), with the split-K workspace slices it asks for."""
+    lib = _lib.load()
+    mode = t.mode
+    d = t.shape.order
+    ext = (ctypes.c_int64 * d)(*t.shape.extents)
+    a_ptr = t.buf.data_ptr()
+    need = lib.tv_tvc_sweep_workspace_bytes(a_ptr, mode.tv_storage, mode.tv_compute, d, ext)
+    if need < 0:
+        raise KernelError("tv_tvc_sweep_workspace_bytes: invalid view")
+    wp, wb, keep = _workspace(need, t.buf.device, stream)
+    xp = (ctypes.c_void_p * d)(*[x.data_ptr() for x in xvs])
+    yp = (ctypes.c_void_p * d)(*[y.data_ptr() for y in ys])
+    _lib.check(lib.tv_tvc_sweep(a_ptr, mode.tv_storage, mode.tv_compute, d, ext, xp, yp, wp, wb,
+                                _lib.stream_ptr(stream)), "tvc sweep")
+    del keep
+
+
 def getvc(
     trans: str,
     alpha: float,

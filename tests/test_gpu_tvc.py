@@ -392,3 +392,32 @@ def test_split_k_workspace_is_caller_provided(tv, oracle, shape, k):
     want = O.tvc(vals, shape, x.cpu().numpy(), k, "f64")
     for y in (y_ws, y_plain, y_api):
         assert np.array_equal(y.cpu().numpy(), want)
+
+
+SWEEP_SHAPES = [(256, 256, 256), (7, 9, 11, 13), (3, 4096, 5), (1 << 14, 3, 40), (979, 33, 2), (2, 3, 1 << 15),
+                (4, 4096, 4096), (96, 96, 96, 96)]
+
+
+@pytest.mark.parametrize("mode_name", ["f64", "f32", "f32f64", "f16f32", "bf16f32"])
+@pytest.mark.parametrize("shape", SWEEP_SHAPES)
+def test_sweep_launch_equals_per_mode_launches(tv, mode_name, shape):
+    """tv_tvc_sweep (one C call, later modes launched with programmatic
+    dependent launch) gives every mode the bits of its own tv_tvc_ws launch,
+    split-K views included, on float data; dtvc_sweep on one slab uses it."""
+    from paper_2501_03121_b200.kernels import launch_sweep
+
+    mode = tv.MODES[mode_name]
+    rng = np.random.default_rng(sum(shape))
+    A = tv.Tensor.from_array(rng.standard_normal(math.prod(shape)).reshape(shape), mode)
+    xs = [tv.demote(rng.standard_normal(n), mode) for n in shape]
+    ys = [torch.empty(A.size // n, dtype=mode.torch_storage, device="cuda") for n in shape]
+    for _ in range(2):  # the second sweep overwrites the first's outputs
+        launch_sweep(A, [tv.kernels._vec(x, mode, "x") for x in xs], ys)
+    torch.cuda.synchronize()
+    for k in range(len(shape)):
+        want = tv.tvc_native(A, xs[k], k).to_numpy()
+        assert np.array_equal(_bits(ys[k].cpu().numpy()), _bits(want)), (k, tv.tvc_regime(A, k))
+    dt = tv.distribute(A, 0, 1)
+    sw = tv.dtvc_sweep(dt, xs)
+    for k in range(len(shape)):
+        assert np.array_equal(_bits(sw[k].parts[0].to_numpy()), _bits(tv.dtvc(dt, xs[k], k).parts[0].to_numpy()))
