@@ -421,3 +421,36 @@ def test_sweep_launch_equals_per_mode_launches(tv, mode_name, shape):
     sw = tv.dtvc_sweep(dt, xs)
     for k in range(len(shape)):
         assert np.array_equal(_bits(sw[k].parts[0].to_numpy()), _bits(tv.dtvc(dt, xs[k], k).parts[0].to_numpy()))
+
+
+@pytest.mark.parametrize("mode_name", ["f64", "f32", "bf16f32"])
+def test_regimes_repeat_bitwise_stress(tv, pinned, mode_name):
+    """The stand-in for racecheck (compute-sanitizer is closed on this pool):
+    every pinned regime -- shared-memory folds of COLS / SLABS, the TMA
+    staged tiles, the norm epilogues -- reruns 25 times on float data with
+    identical bits; a shared-memory race or a missed barrier would show as
+    a run-to-run difference."""
+    mode = tv.MODES[mode_name]
+    rng = np.random.default_rng(17)
+    for shape, k, regime in REGIME_CASES:
+        t = tv.Tensor.from_array(rng.standard_normal(shape), mode)
+        x = tv.demote(rng.standard_normal(shape[k]), mode)
+        pinned(regime)
+        first = tv.tvc_native(t, x, k).buf.clone()
+        outs = [tv.tvc_native(t, x, k).buf for _ in range(25)]
+        for o in outs:
+            assert torch.equal(o.view(torch.int16) if o.dtype == torch.uint16 else o.view(torch.uint8),
+                               first.view(torch.int16) if first.dtype == torch.uint16 else first.view(torch.uint8)), \
+                (shape, k, regime)
+    u, nk, v = 3, 400, 257
+    t = tv.Tensor.from_array(rng.standard_normal((u, nk, v)), mode)
+    x = tv.demote(rng.standard_normal(nk), mode)
+    norms = set()
+    for _ in range(25):
+        out = torch.empty(u * v, dtype=mode.torch_storage, device="cuda")
+        slot = torch.empty(1, dtype=torch.float64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        tv.tvc_normalize_async(t, x, 1, out, slot, None, cnt)
+        norms.add((float(slot.item()), out.view(torch.int16 if out.dtype == torch.uint16 else torch.uint8)
+                   .cpu().numpy().tobytes()))
+    assert len(norms) == 1
