@@ -416,6 +416,7 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
     # outputs read back, through the same public API
     read_gbs = read_stream_gbs(part.buf)
     e2e = run_e2e_sweep(args, tv, dt, part, xs, s, world, rank, group, job_bytes_step)
+    with_asm = run_with_assembly(args, tv, dt, xs, s, world, job_bytes_step) if world > 1 else None
 
     if rank != 0:
         return None
@@ -460,6 +461,7 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
         "dominant_frac_of_read_stream": round(achieved / read_gbs, 4),
         "comm_bytes_per_step_per_gpu": comm_bytes,
         "e2e": e2e,
+        "with_assembly": with_asm,
         "parity": parity,
         "gpu_launches": args.steps * (d + (1 if world > 1 else 0)),
         "step_overlap": "split-mode reduction on a side stream under the other modes" if world > 1 else None,
@@ -579,6 +581,42 @@ def tv_demote_host(v, mode):
     if mode.storage == "brain":
         return (np.asarray(v, np.float32).view(np.uint32) >> 16).astype(np.uint16)
     return np.asarray(v).astype(mode.storage_dtype)
+
+
+def run_with_assembly(args, tv, dt, xs, s, world, job_bytes_step) -> dict:
+    """The reference's dtvc benchmark with --assembly (bench.py:200-215 of the
+    reference): every step's disjoint outputs (k != s) are reassembled into
+    the joint tensor on every rank -- "interleave" by one repack kernel
+    reading the peers' parts over NVLink, "gather-copy" by an NCCL all-gather
+    and a repack.  Same bytes as the plain step (the reference counts no
+    assembly traffic), event-timed, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    out = {}
+    d = dt.order
+    for strategy in ("interleave", "gather-copy"):
+        def astep():
+            res = tv.dtvc_sweep(dt, xs)
+            return [tv.undistribute(res[k], strategy) for k in range(d) if k != s]
+
+        for _ in range(2):
+            astep()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = max(3, min(args.steps, 10))
+        e0.record()
+        for _ in range(n):
+            astep()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / n], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        out[strategy] = {"value": round(job_bytes_step / (ms / 1e3) / 1e9, 2), "unit": "GB/s",
+                         "ms_per_step": round(ms, 4), "steps": n}
+    return out
 
 
 def run_e2e_sweep(args, tv, dt, part, xs, s, world, rank, group, job_bytes_step):

@@ -29,6 +29,7 @@
  *                                       demote(promote+promote) per hop)
  *   tv_peer_barrier comm.py:202-235     the WorkerGroup rendezvous slot + timeout, as a
  *                                       stream-ordered barrier over peer memory
+ *   tv_repack       tensor.py:233-272   reassemble (interleave / gather-copy copy pass)
  *   tv_fill         bench.py:62-80      fill_array (ones / ramp; "hash" replaces numpy's
  *                                       integer-random with a counter hash in [1, 97])
  */
@@ -174,7 +175,10 @@ int tv_normalize(void* x, int storage, int compute, int64_t n, double* norm_out,
  * pointers, p <= TV_MAX_RANKS) into dst (may alias srcs[0]).
  *   mixed == 0: dst[e] = ((s0[e] + s1[e]) + s2[e]) + ...  in the storage type
  *               (exact-width ring_all_reduce, bit-equal to serial_rank_sum)
- *   mixed != 0: with c = chunk ? e / chunk : 0 and r0 = (start + c) % p,
+ *   mixed == 2: dst[e] = demote(((promote(s0[e]) + promote(s1[e])) + ...) in
+ *               the compute type (undistribute's partial-sum collapse,
+ *               hopm.py:76-84; chunk and start ignored)
+ *   mixed == 1: with c = chunk ? e / chunk : 0 and r0 = (start + c) % p,
  *               cur = s_r0[e]; for i in 1..p-1: cur = demote(promote(cur) +
  *               promote(s_{(r0+i)%p}[e]))  (ring_all_reduce_mixed)
  * chunk is ring_chunks' ceil(n/p) for an in-process fold over whole
@@ -212,6 +216,17 @@ int tv_rank_fold_range(const void* src, int64_t src_stride_elems, int p, int64_t
  * peer-memory allreduce, where rank r's buffer holds reduced ring chunk r. */
 int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t chunk, int dtype,
                    void* dst, void* stream);
+
+/* reassemble (tensor.py:233-272): the joint tensor, viewed as (u, ns, v)
+ * around the split mode, from p parts split along it -- part r (a HOST
+ * array of p device pointers; peer pointers work) is (u, ext_r, v) with
+ * ext_r = min(q, ns - r q).  Both assembly strategies end in this one copy
+ * pass: "interleave" passes the parts where they lie, "gather-copy" the
+ * parts' offsets in one gathered buffer.  Bytes are moved as they are
+ * (elem_bytes = 1, 2, 4 or 8), each contiguous run in the widest aligned
+ * unit. */
+int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, int64_t v, int64_t q, int elem_bytes,
+              void* dst, void* stream);
 
 /* Bytes at the start of a peer buffer reserved for the barrier words
  * (uint32 per rank); the transports put their data after it. */

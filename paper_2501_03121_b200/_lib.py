@@ -60,6 +60,7 @@ SIGNATURES = {
                                        _vp]),
     "tv_rank_fold_range": (_int, [_vp, _i64, _int, _i64, _i64, _i64, _int, _int, _int, _vp, _vp]),
     "tv_rank_select": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp]),
+    "tv_repack": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _i64, _i64, _int, _vp, _vp]),
     "tv_peer_barrier": (_int, [ctypes.POINTER(_vp), _int, _int, ctypes.c_uint32, _i64, _vp, _vp]),
     "tv_preload": (_int, [ctypes.POINTER(_int)]),
     "tv_fill": (_int, [_vp, _int, _int, ctypes.c_uint64, ctypes.POINTER(_i64), _int, _int, _i64, _i64, _vp]),

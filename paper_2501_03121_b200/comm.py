@@ -797,6 +797,60 @@ class RankGroup:
         self._end(seq, "all_gather", out.is_cuda)
         return out.view(t.dtype)
 
+    def all_gather_padded(self, rank: int, local: torch.Tensor, counts: list[int]) -> tuple[torch.Tensor, int]:
+        """all_gather without the final compaction: rank r's part sits at
+        [r * q, r * q + counts[r]) of the result, q = max(counts) (what the
+        repack kernel reads)."""
+        self._check_rank(rank)
+        p = self.size
+        seq = self._begin("all_gather")
+        for c in self.counters:
+            c.collective_calls += 1
+        _charge_allgather(self.counters, counts, p)
+        q = max(counts)
+        padded = torch.empty(q, dtype=local.dtype, device=local.device)
+        as_bits(padded[: local.numel()]).copy_(as_bits(local))
+        gathered = torch.empty(p * q, dtype=local.dtype, device=local.device)
+        if p == 1:
+            as_bits(gathered).copy_(as_bits(padded))
+            return gathered, q
+        self._host(seq, "all_gather", self.t.all_gather_into_tensor, _wire(gathered), _wire(padded))
+        self._end(seq, "all_gather", gathered.is_cuda)
+        return gathered, q
+
+    def repack_from_peers(self, local: torch.Tensor, plan, u: int, v: int, out: torch.Tensor) -> bool:
+        """The "interleave" assembly across processes: every rank's part is
+        staged in its peer buffer, then ONE tv_repack reads the p parts
+        straight from the peers (NVLink loads) into the joint tensor ``out``;
+        no NCCL.  False (nothing done) when peer memory is not in use."""
+        from .tensor import repack
+
+        if self.size == 1 or self.algo not in ("fused", "p2p") or not local.is_cuda:
+            return False
+        p = self.size
+        eb = local.element_size()
+        nbytes = max((b - a) for a, b in plan.ranges) * u * v * eb
+        seq = self._begin("all_gather")
+        try:
+            pb = self._peer_buffer(nbytes, local.device)
+        except PeerMemoryUnavailable as exc:
+            warnings.warn(f"RankGroup: {exc}; using algo='exact'")
+            self.algo = "exact"
+            self._issued -= 1
+            return False
+        for c in self.counters:
+            c.collective_calls += 1
+        _charge_allgather(self.counters, [(b - a) * u * v for a, b in plan.ranges], p)
+        self._dev_barrier(pb, "all_gather")  # peers are done with the buffer's previous contents
+        pb.local_data[: local.numel() * eb].copy_(local.view(torch.uint8) if local.dtype != torch.uint16
+                                                 else local.view(torch.int16).view(torch.uint8))
+        self._dev_barrier(pb, "all_gather")  # every part is staged
+        ns = plan.extent
+        repack([pb.data(r) for r in range(p)], p, u, ns, v, plan.chunk, eb, out.data_ptr())
+        self._dev_barrier(pb, "all_gather")  # peers are done reading this rank's part
+        self._end(seq, "all_gather", True)
+        return True
+
     def all_gather(self, rank: int, local: torch.Tensor, counts: list[int] | None = None
                    ) -> torch.Tensor:
         """Rank-order concatenation; ``counts`` gives every rank's length when

@@ -169,6 +169,17 @@ __device__ __forceinline__ void fold_range(const Srcs& srcs, int p, int64_t n, i
   };
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (mixed == 2) {
+    // the partial-sum collapse of undistribute (hopm.py:76-84): promote
+    // every rank's value, add in ascending rank order in the compute type,
+    // demote once
+    for (int64_t e = i0; e < n; e += stride) {
+      C acc = promote<SD, C>(reinterpret_cast<const T*>(srcs.p[0])[e]);
+      for (int r = 1; r < p; ++r) acc = add_rn(acc, promote<SD, C>(reinterpret_cast<const T*>(srcs.p[r])[e]));
+      dst[e] = demote<SD, C>(acc);
+    }
+    return;
+  }
   int64_t done = 0;
   if (vec_ok) {
     const int64_t nv = n / VEC;
@@ -270,6 +281,57 @@ __global__ void k_select(Srcs srcs, int p, int64_t n, int64_t chunk, unsigned ch
     const unsigned char* s = static_cast<const unsigned char*>(srcs.p[r < p ? r : p - 1]);
 #pragma unroll
     for (int b = 0; b < SB; ++b) dst[e * SB + b] = s[e * SB + b];
+  }
+}
+
+// -------------------------------------------------------------- repack ----
+// reassemble (tensor.py:233-272): the joint (u, ns, v) tensor from p parts
+// split along the middle mode, part r = (u, ext_r, v) with ext_r = min(q,
+// ns - r q).  The copy is u * p contiguous runs -- (i, r) moves ext_r * v
+// elements from srcs[r] + i ext_r v to dst + (i ns + r q) v -- taken one run
+// per warp in destination order, each in the widest unit (16, 8, 4, 2 or 1
+// bytes) its source, destination and length allow.
+template <typename U>
+__device__ __forceinline__ void copy_run(const unsigned char* s, unsigned char* d, int64_t len, int lane) {
+  const U* su = reinterpret_cast<const U*>(s);
+  U* du = reinterpret_cast<U*>(d);
+  const int64_t n = len / (int64_t)sizeof(U);
+  int64_t e = lane;
+  if constexpr (sizeof(U) == 16) {
+    for (; e + 96 < n; e += 128) {  // four 16-byte loads in flight per lane
+      const uint4 a = ld_stream16(su + e), b = ld_stream16(su + e + 32), c = ld_stream16(su + e + 64),
+                  f = ld_stream16(su + e + 96);
+      du[e] = a;
+      du[e + 32] = b;
+      du[e + 64] = c;
+      du[e + 96] = f;
+    }
+    for (; e < n; e += 32) du[e] = ld_stream16(su + e);
+  } else {
+    for (; e < n; e += 32) du[e] = su[e];
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_repack(Srcs srcs, int p, int64_t u, int64_t ns, int64_t v, int64_t q, int eb, unsigned char* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t runs = u * p;
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < runs; t += warps) {
+    const int64_t i = t / p;
+    const int r = (int)(t - i * p);
+    const int64_t lo = (int64_t)r * q;
+    const int64_t ext = lo >= ns ? 0 : (q < ns - lo ? q : ns - lo);
+    if (ext == 0) continue;
+    const int64_t len = ext * v * eb;
+    const unsigned char* s = static_cast<const unsigned char*>(srcs.p[r]) + i * len;
+    unsigned char* d = dst + (i * ns + lo) * v * eb;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)len;
+    if ((al & 15) == 0) copy_run<uint4>(s, d, len, lane);
+    else if ((al & 7) == 0) copy_run<uint64_t>(s, d, len, lane);
+    else if ((al & 3) == 0) copy_run<uint32_t>(s, d, len, lane);
+    else if ((al & 1) == 0) copy_run<uint16_t>(s, d, len, lane);
+    else copy_run<unsigned char>(s, d, len, lane);
   }
 }
 
@@ -533,6 +595,29 @@ extern "C" int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t
     default: k_select<2><<<g, 256, 0, st>>>(s, p, n, chunk, d, vec_ok); break;
   }
   return check_launch("tv_rank_select");
+}
+
+extern "C" int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
+                         int elem_bytes, void* dst, void* stream) {
+  using namespace tv;
+  if (!srcs || p < 1 || p > TV_MAX_RANKS || u < 0 || ns < 0 || v < 0 || q < 1 ||
+      (int64_t)(p - 1) * q >= ns + q || !(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8))
+    return set_error(TV_EKERNEL, "tv_repack: bad arguments");
+  if (u == 0 || ns == 0 || v == 0) return TV_OK;
+  if (!dst) return set_error(TV_EKERNEL, "tv_repack: null destination");
+  Srcs s{};
+  for (int r = 0; r < p; ++r) {
+    if (!srcs[r] && (int64_t)r * q < ns) return set_error(TV_EKERNEL, "tv_repack: null source");
+    s.p[r] = srcs[r];
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t runs = u * p;
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((runs + 7) / 8, (int64_t)sms * 8));
+  k_repack<<<g, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(s, p, u, ns, v, q, elem_bytes,
+                                                                   static_cast<unsigned char*>(dst));
+  return check_launch("tv_repack");
 }
 
 extern "C" int tv_fill(void* A, int dtype, int kind, uint64_t seed, const int64_t* ext, int d,

@@ -159,6 +159,16 @@ def run_checks(rank: int, world: int, make_group, tv, O, *, quick: bool = False)
         hosta = O.demote(fulla.reshape(-1), name).reshape(ashape)
         dt = tv.distribute_generated(tv.Shape(ashape), 1, world, mode, fill="hash", seed=9, group=group)
         ok.append((name, "assemble-input", _same(tv.undistribute(dt).to_numpy(), hosta)))
+        # the same through the fused group: interleave = repack straight from
+        # the peers' parts in peer memory; gather-copy = NCCL all-gather + repack
+        dtf = tv.distribute_generated(tv.Shape(ashape), 1, world, mode, fill="hash", seed=9, group=fused)
+        for strategy in ("interleave", "gather-copy"):
+            for _ in range(2):  # twice: the peer buffer is reused
+                got = tv.undistribute(dtf, strategy).to_numpy()
+            ok.append((name, "assemble-peer", strategy, _same(got, hosta)))
+            x = O.demote((np.arange(ashape[0]) % 4) + 1.0, name).copy()
+            got = tv.undistribute(tv.dtvc(dtf, x, 0), strategy).to_numpy()
+            ok.append((name, "assemble-peer-out", strategy, _same(got, O.tvc(hosta.reshape(-1), ashape, x, 0, name))))
         for k in (0, 3):
             x = O.demote((np.arange(ashape[k]) % 4) + 1.0, name).copy()
             got = tv.undistribute(tv.dtvc(dt, x, k)).to_numpy()
@@ -169,6 +179,9 @@ def run_checks(rank: int, world: int, make_group, tv, O, *, quick: bool = False)
         # brain storage truncates each rank's partial sum before the fold
         ok.append((name, "assemble-partial", bool(np.allclose(O.promote(got, name), O.promote(want, name),
                                                               rtol=1e-2 if name == "bf16f32" else 1e-6))))
+        parts_h, ranges_h = O.split(hosta, 1, world)
+        _, pouts, _ = O.dtvc(parts_h, ranges_h, 1, x, 1, name, defer=True)
+        ok.append((name, "assemble-partial-exact", _same(got, O.undistribute_partial(pouts, name))))
 
     # the dHOPM3 reduction with the normalisation in the fold's epilogue:
     # the same bits as all_reduce_sum + normalize

@@ -432,3 +432,30 @@ def test_dhopm3_order4_fp64_split3_twenty_sweeps_96(tv, oracle, p):
     np.testing.assert_allclose(np.asarray(res.norms), np.asarray(norms), rtol=1e-12, atol=0)
     for got, want in zip(res.vectors, vecs):
         assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+
+
+ASSEMBLY_CASES = [((6, 7, 8), 0, 3), ((6, 7, 8), 1, 3), ((6, 7, 8), 2, 3), ((5, 2048, 3), 1, 4),
+                  ((3, 100, 64), 1, 8), ((1000, 3), 0, 7), ((2, 3, 5, 7), 3, 2), ((64, 64, 16), 2, 5)]
+
+
+@pytest.mark.parametrize("name", ["f64", "f32", "f16f32", "bf16f32"])
+@pytest.mark.parametrize("shape,s,p", ASSEMBLY_CASES)
+def test_assembly_repack_both_strategies(tv, oracle, name, shape, s, p):
+    """undistribute / reassemble (tensor.py:233-272, hopm.py:76-84) through
+    tv_repack: interleave and gather-copy both rebuild the tensor bitwise,
+    for 2-, 4- and 8-byte elements, ragged last ranks and runs that are not
+    16-byte multiples; deferred partial sums collapse in the compute type as
+    the oracle does."""
+    O = oracle
+    mode = tv.MODES[name]
+    vals = O.demote(np.random.default_rng(sum(shape) + p).standard_normal(shape).reshape(-1), name).reshape(shape)
+    A = tv.Tensor.from_array(O.promote(vals, name).astype(np.float64), mode)
+    dt = tv.distribute(A, s, p)
+    for strategy in ("interleave", "gather-copy"):
+        got = tv.undistribute(dt, strategy).to_numpy().reshape(shape)
+        assert np.array_equal(got.view(np.uint8), np.ascontiguousarray(vals).view(np.uint8)), strategy
+    x = O.demote(np.random.default_rng(1).standard_normal(shape[s]), name)
+    part = tv.dtvc(dt, x, s, defer=True)
+    got = tv.undistribute(part).to_numpy()
+    want = O.undistribute_partial([q.to_numpy() for q in part.parts], name)
+    assert np.array_equal(got.view(np.uint8), np.ascontiguousarray(want).reshape(-1).view(np.uint8))
