@@ -29,6 +29,10 @@
  *                                       demote(promote+promote) per hop)
  *   tv_peer_barrier comm.py:202-235     the WorkerGroup rendezvous slot + timeout, as a
  *                                       stream-ordered barrier over peer memory
+ *   tv_comm_*       comm.py:168-284    WorkerGroup's ranks, as NCCL communicators
+ *   tv_allreduce    comm.py:84-134      ring_all_reduce / ring_all_reduce_mixed across processes
+ *   tv_allgather    comm.py:137-153     all_gather
+ *   tv_dhopm3_*     hopm.py:229-354     dhopm3 (one sweep per call)
  *   tv_repack       tensor.py:233-272   reassemble (interleave / gather-copy copy pass)
  *   tv_fill         bench.py:62-80      fill_array (ones / ramp; "hash" replaces numpy's
  *                                       integer-random with a counter hash in [1, 97])
@@ -252,6 +256,57 @@ int tv_peer_barrier(void* const* peer_bases, int p, int rank, uint32_t epoch, in
  * rank: call it before the first barrier).  *loaded (may be NULL) receives
  * the number of kernels loaded. */
 int tv_preload(int* loaded);
+
+/* ---- the distributed layer (hopm.py / comm.py without Python) ----------
+ * One NCCL communicator per rank, taken from the process's libnccl.so.2 at
+ * run time.  Either one process per GPU -- rank 0 calls
+ * tv_comm_get_unique_id, ships the 128 bytes to every rank, each calls
+ * tv_comm_init_rank with its device current -- or one process for several
+ * GPUs (tv_comm_init_all, then one host thread per rank).  Collectives are
+ * enqueued on the given stream; every rank must issue the same sequence. */
+#define TV_UNIQUE_ID_BYTES 128
+int tv_comm_get_unique_id(void* id_out);
+int tv_comm_init_rank(const void* id, int nranks, int rank, void** comm_out);
+int tv_comm_init_all(int ndev, const int* devs, void** comms_out);
+int tv_comm_rank_size(void* comm, int* rank, int* size);
+int tv_comm_destroy(void* comm);
+
+/* In-place allreduce of n storage elements (comm.py:84-134):
+ *   TV_AR_EXACT  ascending-rank fold in the storage type (ring_all_reduce)
+ *   TV_AR_MIXED  the mixed ring: chunk c starts at rank c, every hop
+ *                demote(promote + promote) (ring_all_reduce_mixed)
+ *   TV_AR_NCCL   ncclAllReduce (f64/f32 only; rank-consistent, not
+ *                reference-ordered)
+ * EXACT and MIXED give the reference's bits on every rank: NCCL moves the
+ * bytes (small buffers: one all-gather; larger: ring-chunk all-to-all, the
+ * fold of this rank's chunk, all-gather) and tv_rank_fold adds them.  ws:
+ * tv_allreduce_workspace_bytes (allocates nothing). */
+#define TV_AR_NCCL 0
+#define TV_AR_EXACT 1
+#define TV_AR_MIXED 2
+int64_t tv_allreduce_workspace_bytes(void* comm, int64_t n, int storage, int algo);
+int tv_allreduce(void* comm, void* buf, int64_t n, int storage, int compute, int algo, void* ws,
+                 int64_t ws_bytes, void* stream);
+
+/* Rank-order concatenation of counts[r] elements of elem_bytes from every
+ * rank into out (comm.py:137-153 all_gather; parts may differ in length). */
+int tv_allgather(void* comm, const void* local, void* out, const int64_t* counts, int elem_bytes,
+                 void* stream);
+
+/* dHOPM3 (hopm.py:229-354, the reuse schedule of costmodel.py:138-153) on
+ * this rank's slab A of the order-d global tensor ext split along mode s
+ * over the communicator's ranks (comm NULL: one rank, A the whole tensor).
+ * The plan holds the schedule, three rotating product buffers and the
+ * workspaces (allocated here, once).  tv_dhopm3_sweep runs one sweep:
+ * x[0..d-1] (device, full-length vectors in storage format, identical on
+ * every rank) are updated in place, norms_out[j] (device double) gets the
+ * norm of iteration j, status_out (device int32, may be NULL) TV_ENORM on a
+ * zero vector.  Bit-identical to the Python dhopm3 with a RankGroup. */
+int tv_dhopm3_plan_create(void* comm, const void* A, int storage, int compute, int d, const int64_t* ext,
+                          int s, void** plan_out);
+int tv_dhopm3_plan_slab(void* plan, int64_t* lo, int64_t* hi);
+int tv_dhopm3_sweep(void* plan, void* const* x, double* norms_out, int32_t* status_out, void* stream);
+int tv_dhopm3_plan_destroy(void* plan);
 
 /* Fill the rank-local slab [s_lo, s_hi) along mode s of a global tensor with
  * extents ext[0..d-1] (last mode fastest) from the GLOBAL linear index g:

@@ -24,6 +24,7 @@ TV_F64, TV_F32, TV_F16, TV_BF16 = 0, 1, 2, 3
 TV_FILL_ONES, TV_FILL_RAMP, TV_FILL_HASH = 0, 1, 2
 TV_MAX_RANKS = 64
 TV_PEER_HEADER = 4096
+TV_AR_NCCL, TV_AR_EXACT, TV_AR_MIXED = 0, 1, 2
 REGIMES = {0: "naive", 1: "rows", 2: "rows_short", 3: "cols", 4: "slabs", 5: "rows_u", 6: "cols_u",
            7: "slabs_u", 8: "staged", 9: "flat",
            10: "flat_rows", 11: "staged_long"}
@@ -60,6 +61,18 @@ SIGNATURES = {
                                        _vp]),
     "tv_rank_fold_range": (_int, [_vp, _i64, _int, _i64, _i64, _i64, _int, _int, _int, _vp, _vp]),
     "tv_rank_select": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp]),
+    "tv_comm_get_unique_id": (_int, [_vp]),
+    "tv_comm_init_rank": (_int, [_vp, _int, _int, ctypes.POINTER(_vp)]),
+    "tv_comm_init_all": (_int, [_int, ctypes.POINTER(_int), ctypes.POINTER(_vp)]),
+    "tv_comm_rank_size": (_int, [_vp, ctypes.POINTER(_int), ctypes.POINTER(_int)]),
+    "tv_comm_destroy": (_int, [_vp]),
+    "tv_allreduce_workspace_bytes": (_i64, [_vp, _i64, _int, _int]),
+    "tv_allreduce": (_int, [_vp, _vp, _i64, _int, _int, _int, _vp, _i64, _vp]),
+    "tv_allgather": (_int, [_vp, _vp, _vp, ctypes.POINTER(_i64), _int, _vp]),
+    "tv_dhopm3_plan_create": (_int, [_vp, _vp, _int, _int, _int, ctypes.POINTER(_i64), _int, ctypes.POINTER(_vp)]),
+    "tv_dhopm3_plan_slab": (_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "tv_dhopm3_sweep": (_int, [_vp, ctypes.POINTER(_vp), _vp, _vp, _vp]),
+    "tv_dhopm3_plan_destroy": (_int, [_vp]),
     "tv_repack": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _i64, _i64, _int, _vp, _vp]),
     "tv_peer_barrier": (_int, [ctypes.POINTER(_vp), _int, _int, ctypes.c_uint32, _i64, _vp, _vp]),
     "tv_preload": (_int, [ctypes.POINTER(_int)]),

@@ -18,7 +18,7 @@ REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_DIR = PKG_DIR / "_lib"
 LIB_PATH = LIB_DIR / "libtenvec_b200.so"
-SOURCES = ["tvc.cu", "util.cu", "peer.cu"]
+SOURCES = ["tvc.cu", "util.cu", "peer.cu", "dist.cu"]
 HEADERS = ["tv_types.cuh", "tv_internal.h", "tv_norm.cuh"]
 
 NVCC_FLAGS = [
@@ -28,6 +28,7 @@ NVCC_FLAGS = [
     "-lineinfo",
     "-Xcompiler", "-fPIC",
     "-shared",
+    "-ldl",
 ]
 
 

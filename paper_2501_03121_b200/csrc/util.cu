@@ -288,9 +288,17 @@ __global__ void k_select(Srcs srcs, int p, int64_t n, int64_t chunk, unsigned ch
 // reassemble (tensor.py:233-272): the joint (u, ns, v) tensor from p parts
 // split along the middle mode, part r = (u, ext_r, v) with ext_r = min(q,
 // ns - r q).  The copy is u * p contiguous runs -- (i, r) moves ext_r * v
-// elements from srcs[r] + i ext_r v to dst + (i ns + r q) v -- taken one run
-// per warp in destination order, each in the widest unit (16, 8, 4, 2 or 1
-// bytes) its source, destination and length allow.
+// elements from srcs[r] + i ext_r v to dst + (i ns + r q) v -- cut into
+// segments of at most kSeg bytes (a run may be a whole 16 MB slab, or a few
+// bytes); one warp per segment in destination order, each segment in the
+// widest unit (16, 8, 4, 2 or 1 bytes) its source, destination and length
+// allow (segments start at multiples of kSeg, so a run's alignment holds).
+constexpr int64_t kSeg = 32 << 10;
+
+struct RepackRuns {
+  int64_t seg_before[TV_MAX_RANKS + 1];  // prefix sums of segments per run over r (for one i)
+};
+
 template <typename U>
 __device__ __forceinline__ void copy_run(const unsigned char* s, unsigned char* d, int64_t len, int lane) {
   const U* su = reinterpret_cast<const U*>(s);
@@ -313,25 +321,31 @@ __device__ __forceinline__ void copy_run(const unsigned char* s, unsigned char* 
 }
 
 __global__ void __launch_bounds__(256)
-    k_repack(Srcs srcs, int p, int64_t u, int64_t ns, int64_t v, int64_t q, int eb, unsigned char* __restrict__ dst) {
+    k_repack(Srcs srcs, RepackRuns runs, int p, int64_t u, int64_t ns, int64_t v, int64_t q, int eb,
+             unsigned char* __restrict__ dst) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t runs = u * p;
-  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < runs; t += warps) {
-    const int64_t i = t / p;
-    const int r = (int)(t - i * p);
+  const int64_t per_i = runs.seg_before[p];
+  const int64_t total = u * per_i;
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < total; g += warps) {
+    const int64_t i = g / per_i;
+    const int64_t rem = g - i * per_i;
+    int r = 0;
+    while (runs.seg_before[r + 1] <= rem) ++r;
+    const int64_t seg = rem - runs.seg_before[r];
     const int64_t lo = (int64_t)r * q;
-    const int64_t ext = lo >= ns ? 0 : (q < ns - lo ? q : ns - lo);
-    if (ext == 0) continue;
+    const int64_t ext = q < ns - lo ? q : ns - lo;
     const int64_t len = ext * v * eb;
-    const unsigned char* s = static_cast<const unsigned char*>(srcs.p[r]) + i * len;
-    unsigned char* d = dst + (i * ns + lo) * v * eb;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)len;
-    if ((al & 15) == 0) copy_run<uint4>(s, d, len, lane);
-    else if ((al & 7) == 0) copy_run<uint64_t>(s, d, len, lane);
-    else if ((al & 3) == 0) copy_run<uint32_t>(s, d, len, lane);
-    else if ((al & 1) == 0) copy_run<uint16_t>(s, d, len, lane);
-    else copy_run<unsigned char>(s, d, len, lane);
+    const int64_t off = seg * kSeg;
+    const int64_t n = len - off < kSeg ? len - off : kSeg;
+    const unsigned char* s = static_cast<const unsigned char*>(srcs.p[r]) + i * len + off;
+    unsigned char* d = dst + (i * ns + lo) * v * eb + off;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)n;
+    if ((al & 15) == 0) copy_run<uint4>(s, d, n, lane);
+    else if ((al & 7) == 0) copy_run<uint64_t>(s, d, n, lane);
+    else if ((al & 3) == 0) copy_run<uint32_t>(s, d, n, lane);
+    else if ((al & 1) == 0) copy_run<uint16_t>(s, d, n, lane);
+    else copy_run<unsigned char>(s, d, n, lane);
   }
 }
 
@@ -610,12 +624,18 @@ extern "C" int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, 
     if (!srcs[r] && (int64_t)r * q < ns) return set_error(TV_EKERNEL, "tv_repack: null source");
     s.p[r] = srcs[r];
   }
+  RepackRuns runs{};
+  for (int r = 0; r < p; ++r) {
+    const int64_t lo = (int64_t)r * q;
+    const int64_t len = lo >= ns ? 0 : std::min(q, ns - lo) * v * elem_bytes;
+    runs.seg_before[r + 1] = runs.seg_before[r] + (len + kSeg - 1) / kSeg;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t runs = u * p;
-  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((runs + 7) / 8, (int64_t)sms * 8));
-  k_repack<<<g, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(s, p, u, ns, v, q, elem_bytes,
+  const int64_t segs = u * runs.seg_before[p];
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((segs + 7) / 8, (int64_t)sms * 16));
+  k_repack<<<g, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(s, runs, p, u, ns, v, q, elem_bytes,
                                                                    static_cast<unsigned char*>(dst));
   return check_launch("tv_repack");
 }

@@ -39,11 +39,42 @@ def _worker(rank, world, port, q):
         import paper_2501_03121_b200 as tv
 
         ok = multirank_checks.run_checks(rank, world, lambda algo: tv.RankGroup(algo=algo), tv, O)
+        ok += _capi(rank, world, tv)
         q.put((rank, ok))
     except Exception as exc:  # noqa: BLE001
         q.put((rank, [("error", repr(exc)[:500], False)]))
     finally:
         dist.destroy_process_group()
+
+
+def _capi(rank, world, tv):
+    """The distributed C-ABI with one NCCL communicator per process (the
+    unique id travels over torch.distributed, as any launcher would ship it)."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    import capi_checks
+    from paper_2501_03121_b200 import _lib
+
+    lib = _lib.load()
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        _lib.check(lib.tv_comm_get_unique_id(uid), "unique id")
+    box = [bytes(uid.raw)]
+    dist.broadcast_object_list(box, src=0)
+    uid = ctypes.create_string_buffer(box[0], 128)
+    comm = ctypes.c_void_p()
+    _lib.check(lib.tv_comm_init_rank(uid, world, rank, ctypes.byref(comm)), "comm")
+    try:
+        r, n = ctypes.c_int(), ctypes.c_int()
+        lib.tv_comm_rank_size(comm, ctypes.byref(r), ctypes.byref(n))
+        ok = [("capi-comm", r.value == rank and n.value == world)]
+        ok += capi_checks.run_capi_checks(rank, world, tv, comm)
+    finally:
+        torch.cuda.synchronize()
+        lib.tv_comm_destroy(comm)
+    return ok
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
