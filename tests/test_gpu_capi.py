@@ -45,3 +45,58 @@ def test_collectives_with_one_rank_need_a_communicator(tv):
     buf = torch.ones(8, dtype=torch.float64, device="cuda")
     assert lib.tv_allreduce(None, buf.data_ptr(), 8, 0, 0, 1, None, 0, None) != 0
     assert b"communicator" in lib.tv_last_error()
+
+
+def test_c_program_drives_dhopm3_without_python(tv, tmp_path):
+    """examples/dhopm3_capi.c -- a plain C host (gcc, libcudart, this .so;
+    no Python in the process) -- prints the same norms as the package's
+    dhopm3 on the same tensor, to the last bit."""
+    import os
+    import shutil
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    lib_dir = os.path.join(root, "paper_2501_03121_b200", "_lib")
+    exe = str(tmp_path / "dhopm3_capi")
+    subprocess.run([cc, "-O2", "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+                    os.path.join(root, "examples", "dhopm3_capi.c"), "-o", exe, "-L", lib_dir, "-ltenvec_b200",
+                    "-L", "/usr/local/cuda/lib64", "-lcudart", "-lpthread"], check=True)
+    env = dict(os.environ, LD_LIBRARY_PATH=lib_dir + ":/usr/local/cuda/lib64:" + os.environ.get("LD_LIBRARY_PATH", ""))
+    n, sweeps = 96, 4
+    out = subprocess.run([exe, "1", str(n), str(sweeps)], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr
+    norms = [float(v) for v in out.stdout.split("norms")[1].split()]
+    shape = tv.Shape((n, n, n))
+    dt = tv.distribute_generated(shape, 0, 1, tv.F64, fill="hash", seed=1)
+    res = tv.dhopm3(dt, tv.initial_vectors(shape, tv.F64), sweeps=sweeps)
+    assert norms == res.norms[-1]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_c_program_across_gpus_equals_in_process_split(tv, tmp_path):
+    """The same C program over 2 GPUs (tv_comm_init_all, one host thread per
+    GPU, NCCL collectives) gives the bits of the reference's threads-as-ranks
+    run of the same 2-way split (dhopm3 on an in-process distribute)."""
+    import os
+    import shutil
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cc = shutil.which("gcc") or shutil.which("cc")
+    lib_dir = os.path.join(root, "paper_2501_03121_b200", "_lib")
+    exe = str(tmp_path / "dhopm3_capi")
+    subprocess.run([cc, "-O2", "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+                    os.path.join(root, "examples", "dhopm3_capi.c"), "-o", exe, "-L", lib_dir, "-ltenvec_b200",
+                    "-L", "/usr/local/cuda/lib64", "-lcudart", "-lpthread"], check=True)
+    env = dict(os.environ, LD_LIBRARY_PATH=lib_dir + ":/usr/local/cuda/lib64:" + os.environ.get("LD_LIBRARY_PATH", ""))
+    n, sweeps = 128, 3
+    out = subprocess.run([exe, "2", str(n), str(sweeps)], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr
+    norms = [float(v) for v in out.stdout.split("norms")[1].split()]
+    shape = tv.Shape((n, n, n))
+    dt = tv.distribute_generated(shape, 0, 2, tv.F64, fill="hash", seed=1)
+    res = tv.dhopm3(dt, tv.initial_vectors(shape, tv.F64), sweeps=sweeps)
+    assert norms == res.norms[-1]
