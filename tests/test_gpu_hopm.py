@@ -459,3 +459,21 @@ def test_assembly_repack_both_strategies(tv, oracle, name, shape, s, p):
     got = tv.undistribute(part).to_numpy()
     want = O.undistribute_partial([q.to_numpy() for q in part.parts], name)
     assert np.array_equal(got.view(np.uint8), np.ascontiguousarray(want).reshape(-1).view(np.uint8))
+
+
+def test_sweep_graph_host_io_replays_a_whole_end_to_end_step(tv):
+    """SweepGraph(host_io=True): each replay uploads the pinned host vectors,
+    runs the sweep and copies every output to pinned host memory; new host
+    vectors give the eager sweep's bits."""
+    shape = (40, 33, 70)
+    A = tv.Tensor.from_array(np.random.default_rng(3).standard_normal(shape))
+    dt = tv.distribute(A, 0, 1)
+    xs = [np.ones(n) for n in shape]
+    g = tv.SweepGraph(dt, xs, host_io=True)
+    for seed in (1, 2):
+        x2 = [np.random.default_rng(seed + n).standard_normal(n) for n in shape]
+        g.replay(x2)
+        torch.cuda.synchronize()
+        want = tv.dtvc_sweep(dt, x2)
+        for k in range(3):
+            assert np.array_equal(g.host_out[k].numpy(), want[k].parts[0].to_numpy())
