@@ -290,7 +290,7 @@ def run_ours(args) -> dict | None:
     world, rank, local = _setup_dist(args.gpus)
     wl = WORKLOADS[args.workload]
     if wl["kind"] == "hopm":
-        return run_hopm(args, tv, wl, world, rank)
+        return run_hopm(args, tv, wl, world, rank, args.workload)
     line = run_sweep(args, tv, wl, world, rank)
     hw = args.hopm_workload
     if hw == "auto":
@@ -299,7 +299,7 @@ def run_ours(args) -> dict | None:
         # the dHOPM3 half of the metric, on a fresh tensor (the sweep's is freed)
         gc.collect()
         torch.cuda.empty_cache()
-        hline = run_hopm(args, tv, WORKLOADS[hw], world, rank)
+        hline = run_hopm(args, tv, WORKLOADS[hw], world, rank, hw)
         if line is not None:
             line["hopm"] = hline
     return line
@@ -732,7 +732,7 @@ def run_e2e_sweep(args, tv, dt, part, xs, s, world, rank, group, job_bytes_step,
     return out
 
 
-def run_hopm(args, tv, wl, world, rank) -> dict | None:
+def run_hopm(args, tv, wl, world, rank, key: str = "c4") -> dict | None:
     """One dHOPM3 run of ``args.steps`` sweeps through the public ``dhopm3``
     on a device-generated tensor split along wl["s"] over the N GPUs.
 
@@ -843,7 +843,8 @@ def run_hopm(args, tv, wl, world, rank) -> dict | None:
         "per_gpu_gbs": round(value / world, 2),
         "roofline_frac_aggregate": round(value / (peak * world), 4),
         "roofline": {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
-                     "frac": round(dom["gbs"] / peak, 4), "traffic": None,
+                     "frac": round(dom["gbs"] / peak, 4),
+                     "traffic": None if args.shape else _traffic(key, f"k{dom['k']}", world),
                      "kernel": f"tv_tvc k={dom['k']} ({dom['regime']}) on the rank's full slab",
                      "bytes_per_launch": dom["bytes"]},
         "full_slab_passes": kern,
