@@ -113,7 +113,13 @@ struct Unit {
 // a clamped in-range vector so the batch issues without predicates.
 // G (chosen on the host) trades the 128-byte-line count of a warp load
 // (G >= 8) against the log2(G) shuffle levels each row's sum costs.
-template <int SD, typename C, int G, int RS, int QB, bool XS, bool PEEL, bool LONG>
+// XR (short aligned rows): each lane's x values -- the same for every row --
+// are copied from shared memory into registers once, so the fold issues no
+// shared-memory loads; the FMA order is unchanged (same bits).  C5's per-rank
+// slab at p = 8 (rows of 512 bf16, k = 2): 6.20 -> 6.63 TB/s although the
+// 2-byte forms go from 64 to 80 registers (3 CTAs per SM; forcing 4 spills);
+// no other ROWS view changes (profiles/r02_rows_ab/rowxr_*.jsonl).
+template <int SD, typename C, int G, int RS, int QB, bool XS, bool PEEL, bool LONG, bool XR = false>
 __global__ void __launch_bounds__(kThreads)
     k_rows(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
            typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int64_t su, C alpha, C beta,
@@ -170,6 +176,17 @@ __global__ void __launch_bounds__(kThreads)
     }
     return e;
   };
+  static_assert(!XR || (XS && !PEEL && !LONG), "register-resident x: short aligned rows only");
+  C xr[XR ? QPL : 1][VEC];
+  if constexpr (XR) {
+    const int64_t nbr = nk / VEC;
+#pragma unroll
+    for (int t = 0; t < QPL; ++t) {
+      const int64_t q = g + (int64_t)t * G;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) xr[t][e] = q < nbr ? xs[q * VEC + e] : C(0);
+    }
+  }
   for (int64_t row0 = gw * RPW * RS; row0 < u; row0 += warps_total * RPW * RS) {
     C acc[RS][VEC];
 #pragma unroll
@@ -239,7 +256,16 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
           for (int t = 0; t < QPL; ++t) {
             const int64_t q = g + (int64_t)t * G;
-            if (q < nb) fold_vec(buf[r2][t], h + q * VEC, acc[r2]);
+            if constexpr (XR) {
+              if (q < nb) {
+                C a[VEC];
+                unpack<SD, C>(buf[r2][t], a);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) acc[r2][e] = fma(a[e], xr[t][e], acc[r2][e]);
+              }
+            } else {
+              if (q < nb) fold_vec(buf[r2][t], h + q * VEC, acc[r2]);
+            }
           }
           if constexpr (PEEL) acc[r2][0] += fold_edges(rp, h, nb);
         }
@@ -1348,7 +1374,18 @@ static void launch_rows(const void* A, const void* x, void* y, int64_t u, int64_
   const size_t xs_bytes = (size_t)nk * sizeof(C);
   const int64_t rows_per_block = (int64_t)kWarps * (32 / G) * RS;
   const unsigned grid = grid_for(u, rows_per_block, 32);
-  if (xs_bytes <= 96 * 1024) {
+  static const int xr_env = [] {  // TENVEC_B200_ROW_XR=0: x from shared memory, for A/B runs
+    const char* e = getenv("TENVEC_B200_ROW_XR");
+    return e ? atoi(e) : 1;
+  }();
+  constexpr int QPLS = kRowBatch / RS;
+  constexpr bool kXR = !LONG && !PEEL && QPLS * VecN<SD>::N * sizeof(C) <= 128;
+  if (kXR && xr_env != 0 && xs_bytes <= 96 * 1024) {
+    auto kern = k_rows<SD, C, G, RS, kRowBatch, true, PEEL, LONG, kXR>;
+    if (xs_bytes > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs_bytes);
+    launch_k(kern, grid, kThreads, xs_bytes, st, (const T*)A, (const T*)x, (T*)y, u, nk, su, al, be, hb);
+  } else if (xs_bytes <= 96 * 1024) {
     auto kern = k_rows<SD, C, G, RS, (LONG && !PEEL) ? kRowBatchLong : kRowBatch, true, PEEL, LONG>;
     if (xs_bytes > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs_bytes);
