@@ -360,6 +360,8 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
     if clocks:
         clocks.start()
     torch.cuda.synchronize()
+    lib = tv._lib.load()
+    n_launch0 = lib.tv_launch_count()
     last = None
     for i in range(args.steps):
         if flush is not None:
@@ -367,6 +369,9 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
         ev[i][0].record()
         last = step()
         ev[i][1].record()
+    n_launches = lib.tv_launch_count() - n_launch0
+    if sweep_graph is not None:  # replays launch on the device what the capture counted once
+        n_launches = args.steps * sweep_graph.kernels_per_replay
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -464,7 +469,9 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
         "e2e": e2e,
         "with_assembly": with_asm,
         "parity": parity,
-        "gpu_launches": args.steps * (d + (1 if world > 1 else 0)),
+        "gpu_launches": n_launches,
+        "gpu_launches_note": "this library's kernels launched in the timed region on rank 0 (tv_launch_count; "
+                             "a graph replay counts the kernels its capture launched)",
         "step_overlap": "split-mode reduction on a side stream under the other modes" if world > 1 else None,
         "clocks": clk,
     }
@@ -763,9 +770,12 @@ def run_hopm(args, tv, wl, world, rank, key: str = "c4") -> dict | None:
     if clocks:
         clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lib = tv._lib.load()
+    n_launch0 = lib.tv_launch_count()
     e0.record()
     res = tv.dhopm3(dt, x0, sweeps=sweeps)
     e1.record()
+    n_launches = lib.tv_launch_count() - n_launch0
     torch.cuda.synchronize()
     clk = clocks.stop() if clocks else None
     ms = e0.elapsed_time(e1)
@@ -858,6 +868,7 @@ def run_hopm(args, tv, wl, world, rank, key: str = "c4") -> dict | None:
                           "sum A[..., i] prod x_m at 3 sampled i (float64 on the host); e2e rerun "
                           "bit-identical"},
         "tvc_launches": res.tvc_count,
+        "gpu_launches": n_launches,
         "lambda_last": lam,
         "clocks": clk,
     }

@@ -73,6 +73,10 @@ enum { TV_FILL_ONES = 0, TV_FILL_RAMP = 1, TV_FILL_HASH = 2 };
 
 /* Library version string and the kernel regime names (diagnostics). */
 const char* tv_version(void);
+
+/* Kernels this library has launched in this process so far (every launch
+ * site counts itself; a bench reads it around its timed region). */
+unsigned long long tv_launch_count(void);
 const char* tv_last_error(void);
 
 /* Y = alpha * (A x_k x) + beta * Y over the rank-local block view

@@ -80,6 +80,7 @@ SIGNATURES = {
     "tv_axpby": (_int, [ctypes.c_double, _vp, ctypes.c_double, _vp, _int, _int, _i64, _vp]),
     "tv_read_stream": (_int, [_vp, _i64, _vp, _vp]),
     "tv_device_sms": (_int, []),
+    "tv_launch_count": (ctypes.c_ulonglong, []),
 }
 
 _ERRORS = {1: KernelError, 2: ModeError, 3: NormalizationError, 4: CollectiveError, 5: DeviceError}

@@ -96,7 +96,7 @@ extern "C" int tv_peer_barrier(void* const* peer_bases, int p, int rank, uint32_
   }
   k_peer_barrier<<<1, TV_MAX_RANKS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       w, p, rank, epoch, (long long)timeout_ns, status);
-  return check_launch("tv_peer_barrier");
+  return launched("tv_peer_barrier");
 }
 
 // Lazy module loading (the CUDA 12 default) loads a kernel at its first

@@ -48,6 +48,8 @@ inline int dtype_bytes(int dt) {
 
 int set_error(int code, const char* msg);
 int check_launch(const char* what);
+int launched(const char* what);  // check_launch + count one launch
+void count_launch();
 int regime_of(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
 // ws / ws_bytes / ws_given: the split-K workspace (tv_tvc_ws); not given =
 // stream-ordered allocation when the view splits

@@ -68,6 +68,7 @@ static thread_local bool t_pdl = false;
 template <typename... KArgs, typename... Args>
 static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      Args... args) {
+  count_launch();
   if (!t_pdl) {
     kern<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
     return;
@@ -1516,9 +1517,11 @@ static void split_finish(C* ws, const Ws& given, int64_t nch, int64_t u, int64_t
   const int64_t n = u * v;
   if (nch >= 32) {
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 8LL * sm_count()));
+    count_launch();
     k_split_fold<SD, C, true><<<g, 256, 0, st>>>(ws, nch, n, v, (T*)y, al, be, hb);
   } else {
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8LL * sm_count()));
+    count_launch();
     k_split_fold<SD, C, false><<<g, 256, 0, st>>>(ws, nch, n, v, (T*)y, al, be, hb);
   }
   if (!given.given) cudaFreeAsync(ws, st);

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <string>
 
 #include "tv_internal.h"
@@ -24,6 +25,17 @@ static thread_local std::string g_err;
 int set_error(int code, const char* msg) {
   g_err = msg ? msg : "";
   return code;
+}
+
+// kernels this library has launched in this process (tv_launch_count):
+// every launch site counts itself -- util.cu / peer.cu through launched(),
+// tvc.cu through launch_k and its split-K fold
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int launched(const char* what) {
+  count_launch();
+  return check_launch(what);
 }
 
 int check_launch(const char* what) {
@@ -99,7 +111,7 @@ static int convert_from(const void* src, int dst_dt, void* dst, int64_t n, cudaS
     case TV_BF16: k_convert<SRC, TV_BF16><<<g, 256, 0, st>>>((const S*)src, (uint16_t*)dst, n); break;
     default: return set_error(TV_EMODE, "tv_convert: bad destination dtype");
   }
-  return check_launch("tv_convert");
+  return launched("tv_convert");
 }
 
 // ---------------------------------------------------------------- norm ----
@@ -124,7 +136,7 @@ static int norm_dispatch(void* x, int storage, int compute, int64_t n, double* n
     case MODE_BF16F32: k_norm<TV_BF16, float><<<1, kNormThreads, 0, st>>>((uint16_t*)x, n, norm_out, status, do_scale); break;
     default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
   }
-  return check_launch("tv_norm");
+  return launched("tv_norm");
 }
 
 // ---------------------------------------------------------------- fold ----
@@ -253,7 +265,7 @@ static int fold_dispatch(const Srcs& s, int p, int64_t n, int64_t chunk, int sta
     case MODE_BF16F32: k_fold<TV_BF16, float><<<g, 256, 0, st>>>(s, p, n, chunk, start, off, mixed, (uint16_t*)dst, v); break;
     default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
   }
-  return check_launch("tv_rank_fold");
+  return launched("tv_rank_fold");
 }
 
 // -------------------------------------------------------------- select ----
@@ -462,7 +474,7 @@ extern "C" int tv_axpby(double alpha, const void* x, double beta, void* y, int s
     case MODE_BF16F32: k_axpby<TV_BF16, float><<<g, 256, 0, st>>>((uint16_t*)y, (const uint16_t*)x, n, (float)alpha, (float)beta, hb, vec_ok); break;
     default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
   }
-  return check_launch("tv_axpby");
+  return launched("tv_axpby");
 }
 
 extern "C" int tv_read_stream(const void* buf, int64_t bytes, void* sink, void* stream) {
@@ -474,8 +486,10 @@ extern "C" int tv_read_stream(const void* buf, int64_t bytes, void* sink, void* 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   k_read_stream<<<sms * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const uint4*>(buf), bytes / 16, reinterpret_cast<uint32_t*>(sink));
-  return check_launch("tv_read_stream");
+  return launched("tv_read_stream");
 }
+
+extern "C" unsigned long long tv_launch_count(void) { return tv::g_launches.load(); }
 
 extern "C" const char* tv_version(void) { return "tenvec_b200 0.1.0 (sm_100a)"; }
 extern "C" const char* tv_last_error(void) { return tv::g_err.c_str(); }
@@ -552,7 +566,7 @@ extern "C" int tv_rank_fold_normalize(const void* src, int64_t src_stride_elems,
     case MODE_BF16F32: k_fold_norm<TV_BF16, float><<<g, kNormThreads, 0, st>>>(s, p, n, chunk, mixed, (uint16_t*)dst, v, norm_out, status_out, counter); break;
     default: return set_error(TV_EMODE, "invalid (storage, compute) pair");
   }
-  return check_launch("tv_rank_fold_normalize");
+  return launched("tv_rank_fold_normalize");
 }
 
 extern "C" int tv_rank_fold_strided(const void* src, int64_t src_stride_elems, int p, int64_t n,
@@ -608,7 +622,7 @@ extern "C" int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t
     case 4: k_select<4><<<g, 256, 0, st>>>(s, p, n, chunk, d, vec_ok); break;
     default: k_select<2><<<g, 256, 0, st>>>(s, p, n, chunk, d, vec_ok); break;
   }
-  return check_launch("tv_rank_select");
+  return launched("tv_rank_select");
 }
 
 extern "C" int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
@@ -637,7 +651,7 @@ extern "C" int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, 
   const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((segs + 7) / 8, (int64_t)sms * 16));
   k_repack<<<g, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(s, runs, p, u, ns, v, q, elem_bytes,
                                                                    static_cast<unsigned char*>(dst));
-  return check_launch("tv_repack");
+  return launched("tv_repack");
 }
 
 extern "C" int tv_fill(void* A, int dtype, int kind, uint64_t seed, const int64_t* ext, int d,
@@ -662,5 +676,5 @@ extern "C" int tv_fill(void* A, int dtype, int kind, uint64_t seed, const int64_
     case TV_BF16: k_fill<TV_BF16><<<g, 256, 0, st>>>((uint16_t*)A, total, kind, seed, V, q, ext[s], s_lo); break;
     default: return set_error(TV_EMODE, "tv_fill: bad dtype");
   }
-  return check_launch("tv_fill");
+  return launched("tv_fill");
 }

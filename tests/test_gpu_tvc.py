@@ -454,3 +454,23 @@ def test_regimes_repeat_bitwise_stress(tv, pinned, mode_name):
         norms.add((float(slot.item()), out.view(torch.int16 if out.dtype == torch.uint16 else torch.uint8)
                    .cpu().numpy().tobytes()))
     assert len(norms) == 1
+
+
+def test_launch_counter_counts_this_librarys_kernels(tv):
+    """tv_launch_count (bench.py's gpu_launches): one per regime launch, d per
+    mode sweep, split-K views add their fold."""
+    from paper_2501_03121_b200.kernels import launch_sweep
+
+    lib = tv._lib.load()
+    A = tv.Tensor.from_array(np.ones((8, 9, 10)))
+    n0 = lib.tv_launch_count()
+    tv.tvc_native(A, np.ones(9), 1)
+    assert lib.tv_launch_count() - n0 == 1
+    ys = [torch.empty(A.size // n, dtype=torch.float64, device="cuda") for n in (8, 9, 10)]
+    n0 = lib.tv_launch_count()
+    launch_sweep(A, [tv.kernels._vec(np.ones(n), tv.F64, "x") for n in (8, 9, 10)], ys)
+    assert lib.tv_launch_count() - n0 == 3
+    T = tv.Tensor.from_array(np.ones((1, 3_000_000)))  # one long dot product: split-K + fold
+    n0 = lib.tv_launch_count()
+    tv.tvc_native(T, np.ones(3_000_000), 1)
+    assert lib.tv_launch_count() - n0 == 2

@@ -145,7 +145,7 @@ def test_worker_group_rendezvous_errors():
 
 def _header_symbols() -> set[str]:
     text = (ROOT / "include" / "tenvec_b200.h").read_text()
-    return set(re.findall(r"^\s*(?:const char\*|int64_t|int)\s+(tv_\w+)\s*\(", text, flags=re.M))
+    return set(re.findall(r"^\s*(?:const char\*|int64_t|unsigned long long|int)\s+(tv_\w+)\s*\(", text, flags=re.M))
 
 
 def test_library_builds_loads_and_exports_every_header_symbol():
