@@ -305,7 +305,8 @@ int tv_allgather(void* comm, const void* local, void* out, const int64_t* counts
  * x[0..d-1] (device, full-length vectors in storage format, identical on
  * every rank) are updated in place, norms_out[j] (device double) gets the
  * norm of iteration j, status_out (device int32, may be NULL) TV_ENORM on a
- * zero vector.  Bit-identical to the Python dhopm3 with a RankGroup. */
+ * zero vector.  Bit-identical to the Python dhopm3 with a RankGroup.  A
+ * must outlive the plan; call with the communicator's device current. */
 int tv_dhopm3_plan_create(void* comm, const void* A, int storage, int compute, int d, const int64_t* ext,
                           int s, void** plan_out);
 int tv_dhopm3_plan_slab(void* plan, int64_t* lo, int64_t* hi);

@@ -468,6 +468,8 @@ extern "C" int tv_allgather(void* comm, const void* local, void* out, const int6
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" int tv_dhopm3_plan_destroy(void* plan);
+
 extern "C" int tv_dhopm3_plan_create(void* comm, const void* A, int storage, int compute, int d, const int64_t* ext,
                                      int s, void** plan_out) {
   if (!A || !ext || !plan_out || d < 2 || d > 64 || s < 0 || s >= d)
@@ -499,7 +501,7 @@ extern "C" int tv_dhopm3_plan_create(void* comm, const void* A, int storage, int
   h->loc[s] = h->hi - h->lo;
   const int rc = build_schedule(h);
   if (rc != TV_OK) {
-    delete h;
+    tv_dhopm3_plan_destroy(h);  // frees whatever build_schedule allocated
     return rc;
   }
   *plan_out = h;
@@ -526,9 +528,10 @@ extern "C" int tv_dhopm3_sweep(void* plan, void* const* x, double* norms_out, in
 extern "C" int tv_dhopm3_plan_destroy(void* plan) {
   if (!plan) return TV_OK;
   Hopm* h = static_cast<Hopm*>(plan);
-  for (void* b : h->bufs) cudaFree(b);
-  cudaFree(h->ws);
-  cudaFree(h->counter);
+  for (void* b : h->bufs)
+    if (b) cudaFree(b);
+  if (h->ws) cudaFree(h->ws);
+  if (h->counter) cudaFree(h->counter);
   delete h;
   return TV_OK;
 }
