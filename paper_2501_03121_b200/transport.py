@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes
 import datetime
 import itertools
+import warnings
 
 import torch
 
@@ -115,10 +116,9 @@ class TorchTransport:
         name = (self.group or self._dist.group.WORLD).group_name
         t, err = None, None
         try:
-            try:
+            with warnings.catch_warnings():  # deprecated (and unnecessary) from torch 2.11 on
+                warnings.simplefilter("ignore", FutureWarning)
                 symm_mem.enable_symm_mem_for_group(name)
-            except Exception:  # noqa: BLE001 - newer torch enables groups lazily
-                pass
             t = symm_mem.empty(TV_PEER_HEADER + nbytes, dtype=torch.uint8, device=device)
             t[:TV_PEER_HEADER].zero_()
         except Exception as exc:  # noqa: BLE001
