@@ -235,3 +235,56 @@ def test_rank_group_validates_knobs_up_front(monkeypatch):
         RankGroup(transport=_FakeTransport(), timeout=0)
     with pytest.raises(CollectiveError):
         RankGroup(transport=_FakeTransport(), algo="ring")
+
+
+def _reference_tensor_module():
+    """The reference's tensor.py (tensor.py:25-144 is the geometry), from the
+    installed baseline/_ref or the read-only source tree; None when neither
+    is here (the GPU box has neither)."""
+    import importlib
+    import sys
+
+    for path in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (path / "tenvec" / "tensor.py").exists():
+            sys.path.insert(0, str(path))
+            try:
+                return importlib.import_module("tenvec.tensor")
+            except Exception:  # noqa: BLE001
+                return None
+            finally:
+                sys.path.remove(str(path))
+    return None
+
+
+def test_geometry_matches_the_reference_package():
+    """geometry.py restates the reference's integer geometry: the same drop,
+    block view, linear index, division rule and split ranges on random
+    shapes (hypothesis), compared with the reference module itself."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    RT = _reference_tensor_module()
+    if RT is None:
+        pytest.skip("the reference package is not in this container")
+
+    @settings(max_examples=300, deadline=None)
+    @given(st.lists(st.integers(1, 9), min_size=1, max_size=6), st.data())
+    def check(ext, data):
+        k = data.draw(st.integers(0, len(ext) - 1))
+        ours, ref = tv.Shape(tuple(ext)), RT.Shape(tuple(ext))
+        assert ours.size == ref.size and ours.order == ref.order
+        assert ours.drop(k).extents == tuple(ref.drop(k).extents)
+        md, rmd = tv.matricize_dims(ours, k), RT.matricize_dims(ref, k)
+        assert (md.u, md.nk, md.v) == (rmd.u, rmd.nk, rmd.v)
+        idx = tuple(data.draw(st.integers(0, n - 1)) for n in ext)
+        assert tv.linear_index(ours, idx) == RT.linear_index(ref, idx)
+        p = data.draw(st.integers(1, 12))
+        vl = data.draw(st.sampled_from([1, 2, 4, 8]))
+        assert tv.optimal_division(ext[k], p, vl) == tuple(RT.optimal_division(ext[k], p, vl))
+        ours_plan, ref_plan = tv.make_split_plan(ext[k], k, p, vl), RT.make_split_plan(ext[k], k, p, vl)
+        assert ours_plan.p_eff == ref_plan.p_eff and ours_plan.chunk == ref_plan.chunk
+        assert [tuple(r) for r in ours_plan.ranges] == [tuple(r) for r in ref_plan.ranges]
+        text = "x".join(map(str, ext))
+        assert tv.parse_shape(text).extents == tuple(RT.parse_shape(text).extents)
+
+    check()
