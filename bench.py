@@ -47,6 +47,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# one hardware queue per stream (main, owner lanes, side stream, NCCL's), set
+# before any CUDA context exists: a device barrier spinning on one stream must
+# never have another stream's kernel queued behind it
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 WORKLOADS = {
     "c2": dict(desc="C2: 2048^3 fp64 TVC mode sweep k=0,1,2 (dTVC, split s=0 over N GPUs)",
