@@ -1,7 +1,7 @@
 """Collectives: reference ring semantics on device buffers, in one process or
 across processes.
 
-Mirrors pkg/src/tenvec/comm.py:1-284 with two transports:
+Mirrors pkg/src/tenvec/comm.py:1-284 at two levels:
 
 * In-process (every rank's buffer lives in this process, as in the
   reference): ``ring_all_reduce`` / ``ring_all_reduce_mixed`` run ONE fold
@@ -12,14 +12,19 @@ Mirrors pkg/src/tenvec/comm.py:1-284 with two transports:
   the reference.  ``WorkerGroup`` keeps the threads-as-ranks rendezvous
   (comm.py:168-284) on top of them.
 
-* One process per GPU (``RankGroup``, torch.distributed over NCCL/NVLink):
-  the same values from an all-to-all of ring chunks (chunk c of every rank
-  lands on rank c, in the storage format, i.e. reduced precision on the wire
-  for the mixed modes), the same fold kernel on rank c, and an all-gather of
-  the folded chunks.  Traffic equals a ring allreduce's reduce-scatter +
-  all-gather; the result is bit-identical to the reference and to every other
-  rank.  ``algo="nccl"`` uses ncclAllReduce instead (faster for huge
-  buffers, rank-consistent but not reference-ordered).
+* One process per GPU (``RankGroup``): the same values over a transport
+  (transport.py: torch.distributed + symmetric memory, or the one-GPU
+  loopback of thread-ranks).  Default "fused": dtvc's split-mode contraction
+  stores each owner's output range straight into that owner's peer memory,
+  the owner folds with the same kernel and every rank gathers the folded
+  ranges (``tvc_reduce_fused``).  "exact": an all-to-all of ring chunks in
+  the storage format (reduced precision on the wire for the mixed modes),
+  the fold on rank c, an all-gather -- a ring allreduce's traffic.  "p2p":
+  that fold straight from the peers' buffers.  All three are bit-identical
+  to the reference and across ranks; "nccl" (ncclAllReduce) is
+  rank-consistent but not reference-ordered.  Device barriers over peer
+  memory carry the reference's timeout semantics (CollectiveTimeout naming
+  the absent ranks).
 
 Counters follow the reference's ring accounting (comm.py:64-81).
 """
