@@ -2,8 +2,11 @@
 
 Mirrors pkg/src/tenvec/kernels.py:1-254.  ``tvc_native`` and ``getvc`` keep
 the reference signatures, argument checks, ``out``-prefix semantics and
-counters, and run the contraction in libtenvec_b200 (``tv_tvc`` /
-``tv_getvc``): one launch over the (u, n_k, v) view whatever the mode, instead
+counters, and run the contraction in libtenvec_b200 (``tv_tvc_ws`` /
+``tv_getvc_ws``, the split-K workspace from torch's caching allocator, so no
+allocation happens inside the library or a captured graph; ``launch_sweep``
+is a mode sweep in one ``tv_tvc_sweep`` call): one launch over the
+(u, n_k, v) view whatever the mode, instead
 of the reference's BLAS matvec or Python loop of u BLAS vecmats
 (kernels.py:159-166).  ``tasks`` is accepted for API compatibility; the
 output partition across CTAs replaces the serial task blocks
