@@ -583,6 +583,120 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// -------------------------------------------------------------- FLAT_U ----
+// Tall narrow slabs whose rows are NOT 16-byte multiples (v = 7 fp64, v = 12
+// bf16 ...) or are too tall for FLAT's shared-memory x: every (slab, row
+// chunk) is one warp streaming its rows as a flat run of 16-byte vectors.
+// A "group" of G = 32 P VEC elements (P warp loads, one per lane each) is a
+// whole number RG = G / v of rows, so lane l's element (s, k) -- offset
+// (32 s + l) VEC + k in every group -- always sits at the same (row, column)
+// of its group: the lane keeps P x VEC accumulators, reads x at two rows per
+// vector, and at the end the warp folds its G partial sums into column sums
+// through shared memory in row order (a fixed order: reruns reproduce bits).
+// Row chunks of rpc rows (a multiple of RG, so chunks start 16-byte aligned)
+// split the long columns; their sums go to the split-K workspace.
+template <int SD, typename C, int P>
+__global__ void __launch_bounds__(kThreads)
+    k_flat_u(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+             typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int v, int64_t su, C alpha, C beta,
+             int has_beta, int64_t nch, int64_t rpc, C* __restrict__ ws) {
+  PdlScope pdl_scope;
+  using T = typename St<SD>::T;
+  constexpr int VEC = VecN<SD>::N;
+  constexpr int G = 32 * P * VEC;
+  constexpr int UG = P >= 4 ? 1 : 4 / P;  // groups per batch: >= 4 loads in flight per lane
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  C* red = reinterpret_cast<C*>(smem_raw) + (size_t)w * G;  // this warp's RG x v partial sums
+  const int RG = G / v;
+  // where this lane's elements sit in a group: first element's row / column,
+  // and the element k from which a vector's elements belong to the next row
+  int r_s[P], kb_s[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int off = (32 * s + lane) * VEC;
+    r_s[s] = off / v;
+    kb_s[s] = v - (off - r_s[s] * v);
+  }
+  const int64_t items = u * nch;
+  const int64_t warps_total = (int64_t)gridDim.x * kWarps;
+  for (int64_t it = (int64_t)blockIdx.x * kWarps + w; it < items; it += warps_total) {
+    const int64_t i = it / nch;
+    const int64_t ch = it - i * nch;
+    const int64_t r0 = ch * rpc;
+    const int64_t r1 = r0 + rpc < nk ? r0 + rpc : nk;
+    const T* base = A + i * su + r0 * v;  // 16-byte aligned: r0 is a multiple of RG
+    const int64_t ng = (r1 - r0) / RG;
+    C acc[P][VEC];
+#pragma unroll
+    for (int s = 0; s < P; ++s)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[s][e] = C(0);
+    auto fold = [&](const uint4& raw, int s, int64_t row0) {
+      C a[VEC];
+      unpack<SD, C>(raw, a);
+      const int64_t rr = row0 + r_s[s];
+      const C x0 = promote<SD, C>(__ldg(x + rr));
+      const C x1 = kb_s[s] < VEC ? promote<SD, C>(__ldg(x + rr + 1)) : x0;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[s][e] = fma(a[e], e < kb_s[s] ? x0 : x1, acc[s][e]);
+    };
+    int64_t g = 0;
+    for (; g + UG <= ng; g += UG) {
+      uint4 buf[UG][P];
+#pragma unroll
+      for (int q = 0; q < UG; ++q)
+#pragma unroll
+        for (int s = 0; s < P; ++s)
+          buf[q][s] = ld_stream16(reinterpret_cast<const uint4*>(base + (g + q) * G) + 32 * s + lane);
+#pragma unroll
+      for (int q = 0; q < UG; ++q)
+#pragma unroll
+        for (int s = 0; s < P; ++s) fold(buf[q][s], s, r0 + (g + q) * RG);
+    }
+    for (; g < ng; ++g) {
+#pragma unroll
+      for (int s = 0; s < P; ++s)
+        fold(ld_stream16(reinterpret_cast<const uint4*>(base + g * G) + 32 * s + lane), s, r0 + g * RG);
+    }
+    // a partial last group (rows r0 + ng RG .. r1): element by element
+    const int64_t tail_rows = (r1 - r0) - ng * RG;
+    if (tail_rows > 0) {
+      const T* tb = base + ng * G;
+      const int64_t row0 = r0 + ng * RG;
+#pragma unroll
+      for (int s = 0; s < P; ++s)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const int row = r_s[s] + (e >= kb_s[s] ? 1 : 0);
+          if (row < tail_rows) {
+            const C a = promote<SD, C>(ld_stream_elem(tb + (32 * s + lane) * VEC + e));
+            acc[s][e] = fma(a, promote<SD, C>(__ldg(x + row0 + row)), acc[s][e]);
+          }
+        }
+    }
+    // element (s, e) of the group is (row r, column c): park it at red[r v + c]
+    // (a bijection over the group), then column c sums its RG rows in order
+#pragma unroll
+    for (int s = 0; s < P; ++s)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) red[(32 * s + lane) * VEC + e] = acc[s][e];
+    __syncwarp();
+    for (int c = lane; c < v; c += 32) {
+      C sum = red[c];
+      for (int r = 1; r < RG; ++r) sum += red[r * v + c];
+      if (nch > 1) {
+        ws[(i * nch + ch) * v + c] = sum;
+      } else {
+        const int64_t o = i * v + c;
+        y[o] = epilogue<SD, C>(sum, alpha, beta, has_beta != 0, y + o);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ----------------------------------------------------------- FLAT_ROWS ----
 // Short aligned rows (v == 1, nkv 16-byte vectors per row, odd part S of nkv
 // in {1, 3, 5, 7}): the warp streams a block of 32 S vectors (= 32 / g whole
@@ -1265,6 +1379,32 @@ static int forced_regime() {
   return f;
 }
 
+// FLAT_U geometry: P = the warp loads per group (a group of 32 P VEC
+// elements is a whole number of rows), 0 when the width is not supported:
+// at most 128 bytes of accumulators per lane (P VEC values of the widest
+// compute type the storage can have), so P <= 8 for fp64 and <= 4 otherwise
+static int flat_u_period(int64_t v, int vec) {
+  if (v < 2 || v >= 32 || v + 1 < vec) return 0;  // a 16-byte vector spans at most two rows
+  const int d = (int)((32LL * vec) % v);
+  const int P = d == 0 ? 1 : (int)(v / gcd_small((int)v, d));
+  // 128 bytes of accumulators per lane: 4-byte storage may accumulate in
+  // fp64 (f32f64); larger budgets for 2-byte storage compiled to 255
+  // registers with spills
+  const int cbytes = vec <= 4 ? 8 : 4;
+  return (P <= 8 && P * vec * cbytes <= 128) ? P : 0;
+}
+
+// row chunks of a FLAT_U launch: enough (slab, chunk) warps for the GPU,
+// chunks a whole number of groups
+static void flat_u_split(int64_t u, int64_t nk, int64_t v, int vec, int P, int64_t* nch, int64_t* rpc) {
+  const int64_t rg = 32LL * P * vec / v;
+  const int64_t want = cdiv(32LL * sm_count(), u);
+  int64_t n = std::max<int64_t>(1, std::min<int64_t>(want, nk / (8 * rg)));
+  int64_t r = cdiv(cdiv(nk, n), rg) * rg;
+  *rpc = r;
+  *nch = cdiv(nk, r);
+}
+
 static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t v, int64_t su,
                           int64_t sk) {
   const int VEC = 16 / sb;
@@ -1298,6 +1438,10 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   const int64_t rodd = nkv > 0 ? nkv / gcd_small(32, (int)std::min<int64_t>(nkv, 32)) : 0;
   const bool flat_rows_ok = v == 1 && al_rows && contiguous && nkv >= 1 && nkv <= 32 &&
                             (rodd == 1 || rodd == 3 || rodd == 5 || rodd == 7);
+  // FLAT_U: contiguous slabs starting on 16 bytes, narrow rows of any
+  // alignment whose group period is supported
+  const bool flat_u_ok = base_al && contiguous && su_al && v > 1 && flat_u_period(v, VEC) > 0 &&
+                         (int64_t)kWarps * 32 * flat_u_period(v, VEC) * VEC * 8 <= 96 * 1024;
   // a forced regime the view cannot take falls through to the heuristics
   const int forced = forced_regime();
   if (forced > 0) {
@@ -1307,7 +1451,7 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
                     (forced == REG_SLABS && v > 1 && al_cols && v / VEC < 32) ||
                     (forced == REG_COLS_U && v > 1) || (forced == REG_SLABS_U && v > 1 && v < 32) ||
                     (forced == REG_STAGED && stageable) || (forced == REG_FLAT && flat_ok) ||
-                    (forced == REG_FLAT_ROWS && flat_rows_ok) ||
+                    (forced == REG_FLAT_ROWS && flat_rows_ok) || (forced == REG_FLAT_U && flat_u_ok) ||
                     (forced == REG_STAGED_LONG && base_al && contiguous && v > 1 && v <= kLongCols &&
                      v * sb <= stb && u > 1 && nk * 8 <= 96 * 1024);
     if (ok) return forced;
@@ -1322,8 +1466,18 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // narrow or row regime gets about u warps, too few for 148 SMs (a single
   // dot product would run on one warp)
   if (u < 16LL * sm_count() && nk >= 8192 && v == 1) return REG_SLABS_U;
-  if (u < 16LL * sm_count() && nk >= 1024 && v > 1 && (al_cols ? v / VEC < 32 : v < 32))
+  if (u < 16LL * sm_count() && nk >= 1024 && v > 1 && (al_cols ? v / VEC < 32 : v < 32)) {
+    static const int fu_env = [] {  // TENVEC_B200_FLAT_U=0: keep SLABS for tall views, for A/B runs
+      const char* e = getenv("TENVEC_B200_FLAT_U");
+      return e ? atoi(e) : 1;
+    }();
+    // FLAT_U beats the scalar 2-byte loads of SLABS_U (C5-like bf16 / f16
+    // narrow rows: [8, 1e6, 12] bf16 1.02 -> 2.32 TB/s); for 4- and 8-byte
+    // storage and aligned rows SLABS / SLABS_U measured as fast or faster
+    // (profiles/r02_flat_u_ab/)
+    if (flat_u_ok && fu_env != 0 && sb == 2 && !al_cols) return REG_FLAT_U;
     return al_cols ? REG_SLABS : REG_SLABS_U;
+  }
   if (v == 1) {
     // rows of 3, 5, 6, 7 vectors idle 25-60 % of ROWS' power-of-two lane
     // groups; streamed flat they measured 6.2-6.35 vs 4.6-5.9 TB/s.  fp64
@@ -1678,6 +1832,11 @@ static int64_t ws_bytes_typed(const void* A, int64_t u, int64_t nk, int64_t v, i
     case REG_COLS_U: nch = cols_split(cols_blocks<SD, false>(u, nk, v, nullptr, nullptr), nk); break;
     case REG_SLABS:
     case REG_SLABS_U: nch = slabs_split(u, nk); break;
+    case REG_FLAT_U: {
+      int64_t rpc = nk;
+      flat_u_split(u, nk, v, (int)VecN<SD>::N, flat_u_period(v, (int)VecN<SD>::N), &nch, &rpc);
+      break;
+    }
     default: break;
   }
   return nch > 1 ? u * nch * v * (int64_t)sizeof(C) : 0;
@@ -1752,6 +1911,32 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       };
       if (P == 1) go(k_flat<SD, C, 1, 8>);
       else go(k_flat<SD, C, 3, 2>);
+      break;
+    }
+    case REG_FLAT_U: {
+      const int P = flat_u_period(v, VEC);
+      int64_t nch = 1, rpc = nk;
+      flat_u_split(u, nk, v, VEC, P, &nch, &rpc);
+      C* ws = nullptr;
+      if (nch > 1 && (ws = split_ws<C>(wsa, u * nch * v, st, &rc)) == nullptr) return rc;
+      const size_t smem = (size_t)kWarps * 32 * P * VEC * sizeof(C);
+      const unsigned grid = grid_for(u * nch, kWarps, 32);
+      auto go = [&](auto kern) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        launch_k(kern, grid, kThreads, smem, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v, su, al, be, hb,
+                 nch, rpc, ws);
+      };
+      switch (P) {
+        case 1: go(k_flat_u<SD, C, 1>); break;
+        case 2: go(k_flat_u<SD, C, 2>); break;
+        case 3: go(k_flat_u<SD, C, 3>); break;
+        case 4: go(k_flat_u<SD, C, 4>); break;
+        case 5: if constexpr (VEC <= 2) go(k_flat_u<SD, C, 5>); break;
+        case 6: if constexpr (VEC <= 2) go(k_flat_u<SD, C, 6>); break;
+        case 7: if constexpr (VEC <= 2) go(k_flat_u<SD, C, 7>); break;
+        default: if constexpr (VEC <= 2) go(k_flat_u<SD, C, 8>); break;
+      }
+      if (ws != nullptr) split_finish<SD, C>(ws, wsa, nch, u, v, y, al, be, hb, st);
       break;
     }
     case REG_SLABS:

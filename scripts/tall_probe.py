@@ -17,7 +17,8 @@ def main() -> int:
     cases = [((4_000_000, 8), 0, "f64"), ((1_000_000, 4, 4), 0, "f64"), ((1, 8_000_000, 16), 1, "f32"),
              ((1_000_000, 100), 0, "f64"), ((2, 2_000_000, 24), 1, "f32"), ((3_000_001, 7), 0, "f64"),
              ((400_000, 64), 0, "f64"), ((200_000, 300), 0, "f64"), ((30623, 30623), 0, "f64"),
-             ((8, 1_000_000, 12), 1, "bf16f32")]
+             ((8, 1_000_000, 12), 1, "bf16f32"), ((8, 1_000_000, 12), 1, "f16f32"),
+             ((3_000_001, 7), 0, "bf16f32"), ((2, 2_000_000, 6), 1, "bf16f32"), ((1_000_003, 20), 0, "f16f32")]
     for shape, k, mname in cases:
         mode = tv.MODES[mname]
         t = tv.distribute_generated(tv.Shape(shape), 0, 1, mode, fill="hash", seed=1).parts[0]
