@@ -139,7 +139,8 @@ int tv_tvc_normalize(const void* A, int storage, int compute, int64_t u, int64_t
  * 3 columns, 4 narrow slabs, and their unaligned (scalar-load) forms 5 rows,
  * 6 columns, 7 slabs, 8 slabs staged through shared memory by TMA bulk
  * copies, 9 flat narrow slabs, 10 flat short rows, 11 larger unaligned slabs
- * as TMA row-run tiles (0 is the naive kernel,
+ * as TMA row-run tiles, 12 tall narrow slabs of any row alignment as flat
+ * 16-byte runs (0 is the naive kernel,
  * tv_tvc_naive only); -1 on invalid arguments. */
 int tv_tvc_regime(const void* A, int storage, int64_t u, int64_t nk, int64_t v);
 
