@@ -38,6 +38,14 @@ def oracle():
 
 
 @pytest.fixture(scope="session")
+def tv_host():
+    """The product package for host-only logic (no device needed)."""
+    import paper_2501_03121_b200 as pkg
+
+    return pkg
+
+
+@pytest.fixture(scope="session")
 def tv():
     """The product package with its CUDA library loaded (GPU tests only)."""
     import torch
