@@ -477,3 +477,33 @@ def test_sweep_graph_host_io_replays_a_whole_end_to_end_step(tv):
         want = tv.dtvc_sweep(dt, x2)
         for k in range(3):
             assert np.array_equal(g.host_out[k].numpy(), want[k].parts[0].to_numpy())
+
+
+@pytest.mark.parametrize("vl", [2, 4, 8])
+def test_vector_length_splits(tv, oracle, vl):
+    """distribute(..., vl): chunks promoted to vector-length multiples
+    (tensor.py:105-118, the C3 trap: 96 over 8 ranks with vl = 8 is 6 ranks
+    of 16) -- dtvc in every mode and a dHOPM3 run on such a split match the
+    oracle's split of the same plan."""
+    O = oracle
+    shape = (96, 10, 12)
+    vals = O.fill_values(shape, "hash", seed=vl).reshape(shape)
+    A = tv.Tensor.from_array(vals)
+    dt = tv.distribute(A, 0, 8, vl)
+    q, pe = O.optimal_division(96, 8, vl)
+    assert dt.plan.p_eff == pe and dt.plan.chunk == q
+    parts, ranges = O.split(vals, 0, 8, vl)
+    for k in range(3):
+        x = (np.arange(shape[k]) % 5) + 1.0
+        _, outs, _ = O.dtvc(parts, ranges, 0, x, k, "f64")
+        got = tv.dtvc(dt, x, k)
+        if k == 0:
+            assert np.array_equal(got.parts[0].to_numpy(), np.asarray(outs[0]).reshape(-1))
+        else:
+            for r in range(pe):
+                assert np.array_equal(got.parts[r].to_numpy(), np.asarray(outs[r]).reshape(-1))
+    x0 = O.initial_vectors(shape, "f64")
+    res = tv.dhopm3(dt, [v.copy() for v in x0], sweeps=3)
+    one = tv.dhopm3(tv.distribute(A, 0, 1), [v.copy() for v in x0], sweeps=3)
+    for a, b in zip(res.vectors, one.vectors):
+        assert np.allclose(a, b, rtol=1e-12, atol=1e-14)
