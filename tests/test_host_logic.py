@@ -195,6 +195,9 @@ def test_library_argument_validation_without_gpu():
     assert lib.tv_tvc_regime(p, 0, 100000, 10, 1000) == 11  # aligned short columns -> row-run tiles
     assert lib.tv_tvc_regime(p, 0, 2048, 2048, 4096) == 3  # aligned long columns stay COLS
     assert lib.tv_tvc_regime(p, 0, 979, 979, 979) == 6     # too few slabs to balance -> scalar columns
+    assert lib.tv_tvc_regime(p, 3, 8, 1000000, 12) == 12   # tall unaligned bf16 slabs -> flat runs
+    assert lib.tv_tvc_regime(p, 1, 8, 1000000, 12) == 4    # the same in fp32 (aligned) -> slabs
+    assert lib.tv_tvc_regime(p, 0, 1, 3000001, 7) == 7     # tall unaligned fp64 -> scalar slabs
     # the diagnostic override pins a regime only where the view can take it
     prev = lib.tv_set_regime_override(1)
     try:
@@ -203,6 +206,32 @@ def test_library_argument_validation_without_gpu():
     finally:
         lib.tv_set_regime_override(prev)
     assert lib.tv_tvc_regime(p, 1, 1000, 96, 1) == 8
+
+
+def test_distributed_cabi_validates_arguments_without_gpu():
+    """The distributed C-ABI rejects bad calls before touching a device or
+    NCCL (include/tenvec_b200.h): null plans / communicators, bad modes and
+    splits, bad repack geometry; destroying NULL is a no-op."""
+    lib = _lib.load()
+    plan = ctypes.c_void_p()
+    ext = (ctypes.c_int64 * 3)(4, 5, 6)
+    assert lib.tv_dhopm3_plan_create(None, None, 0, 0, 3, ext, 0, ctypes.byref(plan)) == 1
+    assert lib.tv_dhopm3_plan_create(None, 1 << 20, 0, 0, 3, ext, 3, ctypes.byref(plan)) == 1  # s out of range
+    assert lib.tv_dhopm3_plan_create(None, 1 << 20, 2, 2, 3, ext, 0, ctypes.byref(plan)) == 2  # f16 compute
+    assert lib.tv_dhopm3_sweep(None, None, None, None, None) == 1
+    assert lib.tv_dhopm3_plan_destroy(None) == 0 and lib.tv_comm_destroy(None) == 0
+    assert lib.tv_allreduce(None, None, 8, 0, 0, 1, None, 0, None) == 4
+    assert lib.tv_allreduce_workspace_bytes(None, 8, 0, 1) == -1
+    assert lib.tv_allgather(None, None, None, None, 8, None) == 4
+    assert lib.tv_comm_rank_size(None, None, None) == 4
+    assert lib.tv_comm_init_rank(None, 2, 0, ctypes.byref(plan)) == 4
+    srcs = (ctypes.c_void_p * 2)(1 << 20, 1 << 21)
+    assert lib.tv_repack(srcs, 2, 1, 10, 1, 0, 8, 1 << 22, None) == 1     # chunk q = 0
+    assert lib.tv_repack(srcs, 2, 1, 10, 1, 5, 3, 1 << 22, None) == 1     # 3-byte elements
+    assert lib.tv_repack(srcs, 2, 0, 10, 1, 5, 8, None, None) == 0       # empty: nothing to do
+    bases = (ctypes.c_void_p * 2)(1 << 20, 1 << 21)
+    assert lib.tv_peer_barrier(bases, 2, 2, 1, 0, None, None) == 4         # rank out of range
+    assert lib.tv_launch_count() >= 0
 
 
 def test_no_oracle_import_in_product():
