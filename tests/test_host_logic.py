@@ -317,3 +317,50 @@ def test_geometry_matches_the_reference_package():
         assert tv.parse_shape(text).extents == tuple(RT.parse_shape(text).extents)
 
     check()
+
+
+def _fold_range_host(slots, p, n, ring_chunk, offset, mode, mixed, O):
+    """numpy restatement of tv_rank_fold_range: element e of the range is
+    global index offset + e; the mixed ring starts it at rank
+    ((offset + e) // ring_chunk) % p (include/tenvec_b200.h)."""
+    out = np.empty(n, dtype=slots[0].dtype)
+    for e in range(n):
+        r0 = ((offset + e) // ring_chunk) % p if mixed else 0
+        cur = slots[r0][e]
+        for i in range(1, p):
+            b = slots[(r0 + i) % p][e]
+            cur = O.demote(O.promote(np.array([cur]), mode) + O.promote(np.array([b]), mode), mode)[0] \
+                if mixed or O.MODES[mode][2] or O.MODES[mode][0] != O.MODES[mode][1] else cur + b
+        out[e] = cur
+    return out
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5])
+def test_fused_plan_index_math_on_host(oracle, p):
+    """RankGroup's fused split-mode reduction, its index math restated on
+    the host (fused_plan's owner ranges and slots, the owner fold over its
+    range, the select over the owners): every rank's partial sums -- the
+    oracle's -- reduce to exactly the reference's exact / mixed ring result,
+    for slab owners (u >= p, ragged and empty last owners) and column owners
+    (u == 1)."""
+    from paper_2501_03121_b200.comm import fused_plan
+
+    O = oracle
+    rng = np.random.default_rng(p)
+    for u, v in ((p * 3 + 1, 5), (p, 7), (p + 2, 1), (1, 13 * p + 3), (1, p)):
+        plan = fused_plan(u, v, p, 8)
+        assert plan is not None
+        n = u * v
+        for mode in ("f64", "bf16f32", "f16f32"):
+            mixed = O.is_mixed(mode)
+            partials = [O.demote(rng.uniform(-4, 4, n), mode) for _ in range(p)]
+            want = O.fold_mixed([q.copy() for q in partials], mode) if mixed else O.fold_exact(partials)
+            folded = []
+            for c in range(p):
+                lo, hi = plan.bounds[c]
+                a, b = lo * plan.unit, hi * plan.unit
+                assert b - a == plan.sizes[c]
+                slots = [q[a:b] for q in partials]  # rank r's owner-c range, as it lands in slot r
+                folded.append(_fold_range_host(slots, p, b - a, plan.ring_chunk, c * plan.chunk, mode, mixed, O))
+            got = np.concatenate(folded)  # tv_rank_select: chunk c from owner c
+            assert np.array_equal(got.view(np.uint8), np.asarray(want).view(np.uint8)), (u, v, mode)
