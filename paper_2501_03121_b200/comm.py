@@ -692,6 +692,28 @@ class RankGroup:
             self._end(seq, "dtvc_reduce", True)
         return out
 
+    def native_comm(self) -> int:
+        """This rank's NCCL communicator for the C-ABI's distributed entry
+        points (tv_comm_init_rank), created on first use: rank 0's unique id
+        travels through the group's store.  One process per GPU only."""
+        if getattr(self, "_native_comm", None):
+            return self._native_comm
+        store = getattr(self.t, "store", None)
+        if store is None or getattr(self.t, "backend", "") != "nccl":
+            raise CollectiveError("native collectives need one process per GPU over NCCL (a c10d store)")
+        lib = _lib.load()
+        key = f"tenvec_b200/{self.t.gid}/nccl_unique_id"
+        if self.rank == 0:
+            uid = ctypes.create_string_buffer(128)
+            _lib.check(lib.tv_comm_get_unique_id(uid), "native comm")
+            store.set(key, bytes(uid.raw))
+        raw = store.get(key)
+        comm = ctypes.c_void_p()
+        _lib.check(lib.tv_comm_init_rank(ctypes.create_string_buffer(bytes(raw), 128), self.size, self.rank,
+                                         ctypes.byref(comm)), "native comm")
+        self._native_comm = comm.value
+        return self._native_comm
+
     # -- host-ordered collectives ----------------------------------------------
     def _check_rank(self, rank: int) -> None:
         if rank != self.rank:

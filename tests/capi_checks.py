@@ -61,6 +61,21 @@ def run_capi_checks(rank: int, world: int, tv, comm) -> list:
         res = tv.dhopm3(dt, [v.copy() for v in x0], sweeps=3)
         vecs, norms, st = c_dhopm3(tv, comm, dt.parts[rank], shape, s, mode, x0, 3)
         ok.append(("capi-dhopm3", shape, s, name, st == 0 and same_run(res, vecs, norms)))
+    # dhopm3(native=True) across the group: the C++ plan on a communicator
+    # of its own, the Python driver's bits and counters
+    for shape, s, name in [((world * 4, 10, 9), 0, "f64"), ((6, world * 5, 7), 1, "bf16f32")]:
+        mode = tv.MODES[name]
+        dt = tv.distribute_generated(tv.Shape(shape), s, world, mode, fill="hash", seed=6, group=group)
+        x0 = tv.initial_vectors(tv.Shape(shape), mode)
+        before = [(c.collective_calls, c.touched_elements) for c in group.counters]
+        py = tv.dhopm3(dt, [v.copy() for v in x0], sweeps=2)
+        mid = [(c.collective_calls, c.touched_elements) for c in group.counters]
+        nat = tv.dhopm3(dt, [v.copy() for v in x0], sweeps=2, native=True)
+        after = [(c.collective_calls, c.touched_elements) for c in group.counters]
+        same_counts = all((m[0] - b0[0], m[1] - b0[1]) == (a[0] - m[0], a[1] - m[1])
+                          for b0, m, a in zip(before, mid, after))
+        ok.append(("native-dhopm3", shape, name, same_run(py, nat.vectors, nat.norms) and same_counts
+                   and nat.iteration_touched == py.iteration_touched))
     # allreduce: small (one gather) and large (chunk exchange) buffers
     for n in (1001, 600_003):
         for name, algo in (("f64", _lib.TV_AR_EXACT), ("f32", _lib.TV_AR_EXACT), ("bf16f32", _lib.TV_AR_MIXED),

@@ -507,3 +507,33 @@ def test_vector_length_splits(tv, oracle, vl):
     one = tv.dhopm3(tv.distribute(A, 0, 1), [v.copy() for v in x0], sweeps=3)
     for a, b in zip(res.vectors, one.vectors):
         assert np.allclose(a, b, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("name", ["f64", "f32", "f32f64", "f16f32", "bf16f32"])
+@pytest.mark.parametrize("shape,s", [((12, 10, 9), 0), ((6, 7, 8, 5), 2), ((3, 4, 5, 6, 2), 4), ((64, 2048, 3), 1)])
+def test_native_dhopm3_equals_the_python_driver(tv, name, shape, s):
+    """dhopm3(native=True): the C++ rank body drives the sweeps; vectors,
+    norms, TVC counts and every counter equal the Python driver's."""
+    mode = tv.MODES[name]
+    A = tv.Tensor.from_array(np.random.default_rng(sum(shape)).standard_normal(shape), mode)
+    x0 = tv.initial_vectors(tv.Shape(shape), mode)
+    py = tv.dhopm3(tv.distribute(A, s, 1), [v.copy() for v in x0], sweeps=3)
+    nat = tv.dhopm3(tv.distribute(A, s, 1), [v.copy() for v in x0], sweeps=3, native=True)
+    assert nat.norms == py.norms
+    assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(nat.vectors, py.vectors))
+    assert (nat.tvc_count, nat.tvc_per_sweep) == (py.tvc_count, py.tvc_per_sweep)
+    assert nat.iteration_touched == py.iteration_touched
+    a, b = nat.kernel_counters[0], py.kernel_counters[0]
+    assert (a.elements_read, a.elements_written, a.bytes_touched, a.invocations) == \
+        (b.elements_read, b.elements_written, b.bytes_touched, b.invocations)
+    assert [c.collective_calls for c in nat.comm_counters] == [c.collective_calls for c in py.comm_counters]
+
+
+def test_native_dhopm3_rejects_what_it_cannot_run(tv):
+    A = tv.Tensor.from_array(np.ones((4, 5, 6)))
+    with pytest.raises(tv.ContractError):
+        tv.dhopm3(tv.distribute(A, 0, 2), sweeps=1, native=True)  # two ranks in one process
+    with pytest.raises(tv.ContractError):
+        tv.dhopm3(tv.distribute(A, 0, 1), sweeps=1, native=True, reuse=False)
+    with pytest.raises(tv.NormalizationError):
+        tv.dhopm3(tv.distribute(tv.Tensor.from_array(np.zeros((4, 5, 6))), 0, 1), sweeps=1, native=True)
