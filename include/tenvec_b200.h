@@ -237,6 +237,12 @@ int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t chunk, int
 int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, int64_t v, int64_t q, int elem_bytes,
               void* dst, void* stream);
 
+/* One part's share of tv_repack: part r's runs from src into the joint
+ * tensor at dst (which may be a peer's buffer: the interleave assembly
+ * across GPUs pushes every rank's part into every rank's joint copy). */
+int tv_repack_part(const void* src, int r, int p, int64_t u, int64_t ns, int64_t v, int64_t q, int elem_bytes,
+                   void* dst, void* stream);
+
 /* Bytes at the start of a peer buffer reserved for the barrier words
  * (uint32 per rank); the transports put their data after it. */
 #define TV_PEER_HEADER 4096

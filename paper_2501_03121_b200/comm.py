@@ -846,17 +846,16 @@ class RankGroup:
         return gathered, q
 
     def repack_from_peers(self, local: torch.Tensor, plan, u: int, v: int, out: torch.Tensor) -> bool:
-        """The "interleave" assembly across processes: every rank's part is
-        staged in its peer buffer, then ONE tv_repack reads the p parts
-        straight from the peers (NVLink loads) into the joint tensor ``out``;
-        no NCCL.  False (nothing done) when peer memory is not in use."""
-        from .tensor import repack
-
+        """The "interleave" assembly across processes: every rank PUSHES its
+        part's runs straight into every rank's joint copy in peer memory
+        (tv_repack_part; NVLink stores are posted, loads would pay a round
+        trip each), then copies its own joint copy out; no NCCL.  False
+        (nothing done) when peer memory is not in use."""
         if self.size == 1 or self.algo not in ("fused", "p2p") or not local.is_cuda:
             return False
         p = self.size
         eb = local.element_size()
-        nbytes = max((b - a) for a, b in plan.ranges) * u * v * eb
+        nbytes = out.numel() * eb
         seq = self._begin("all_gather")
         try:
             pb = self._peer_buffer(nbytes, local.device)
@@ -868,13 +867,16 @@ class RankGroup:
         for c in self.counters:
             c.collective_calls += 1
         _charge_allgather(self.counters, [(b - a) * u * v for a, b in plan.ranges], p)
-        self._dev_barrier(pb, "all_gather")  # peers are done with the buffer's previous contents
-        pb.local_data[: local.numel() * eb].copy_(local.view(torch.uint8) if local.dtype != torch.uint16
-                                                 else local.view(torch.int16).view(torch.uint8))
-        self._dev_barrier(pb, "all_gather")  # every part is staged
-        ns = plan.extent
-        repack([pb.data(r) for r in range(p)], p, u, ns, v, plan.chunk, eb, out.data_ptr())
-        self._dev_barrier(pb, "all_gather")  # peers are done reading this rank's part
+        self._dev_barrier(pb, "all_gather")  # every rank is done with its joint copy's previous contents
+        lib = _lib.load()
+        stream = _lib.stream_ptr()
+        for j in range(p):  # own copy first, then the peers in ring order
+            c = (self.rank + j) % p
+            _lib.check(lib.tv_repack_part(local.data_ptr(), self.rank, p, u, plan.extent, v, plan.chunk, eb,
+                                          pb.data(c), stream), "interleave assembly")
+        self._dev_barrier(pb, "all_gather")  # every part has landed in every joint copy
+        out.view(torch.uint8).copy_(pb.local_data[:nbytes]) if out.dtype != torch.uint16 else \
+            out.view(torch.int16).view(torch.uint8).copy_(pb.local_data[:nbytes])
         self._end(seq, "all_gather", True)
         return True
 

@@ -361,6 +361,35 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Short runs (a split along the last modes: C3's 96-wide rows cut in 48 or
+// 24-element parts are 96-192 B runs): one thread per 16-byte unit instead
+// of a warp per run.  Whole-tensor form (only < 0): thread t writes
+// destination unit t -- row i = t / upr, part r, offset -- coalesced stores;
+// one-part form (only = r): thread t reads part r's unit t and stores it at
+// its place in the joint row (the push of the interleave assembly).
+// 32-bit unit indices (the host checks the launch fits).
+__global__ void __launch_bounds__(256)
+    k_repack_units(Srcs srcs, int p, int only, uint32_t total, uint32_t upr, uint32_t qu, uint32_t lastu,
+                   uint4* __restrict__ dst) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    if (only < 0) {
+      const uint32_t i = t / upr;
+      const uint32_t rem = t - i * upr;
+      uint32_t r = rem / qu;
+      if (r > (uint32_t)(p - 1)) r = p - 1;
+      const uint32_t off = rem - r * qu;
+      const uint32_t ext = r == (uint32_t)(p - 1) ? lastu : qu;
+      dst[t] = ld_stream16(static_cast<const uint4*>(srcs.p[r]) + (size_t)i * ext + off);
+    } else {
+      const uint32_t ext = only == p - 1 ? lastu : qu;
+      const uint32_t i = t / ext;
+      const uint32_t off = t - i * ext;
+      dst[(size_t)i * upr + (size_t)only * qu + off] = ld_stream16(static_cast<const uint4*>(srcs.p[only]) + t);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- fill ----
 __host__ __device__ inline uint64_t fill_hash(uint64_t seed, uint64_t g) {
   uint64_t z = (g + 1ULL) * 0x9E3779B97F4A7C15ULL + seed * 0xD1B54A32D192ED03ULL;
@@ -625,8 +654,24 @@ extern "C" int tv_rank_select(const void* const* srcs, int p, int64_t n, int64_t
   return launched("tv_rank_select");
 }
 
+static int repack_impl(const void* const* srcs, int p, int only, int64_t u, int64_t ns, int64_t v, int64_t q,
+                       int elem_bytes, void* dst, void* stream);
+
 extern "C" int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
                          int elem_bytes, void* dst, void* stream) {
+  return repack_impl(srcs, p, -1, u, ns, v, q, elem_bytes, dst, stream);
+}
+
+extern "C" int tv_repack_part(const void* src, int r, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
+                              int elem_bytes, void* dst, void* stream) {
+  if (r < 0 || r >= p || p > TV_MAX_RANKS) return tv::set_error(TV_EKERNEL, "tv_repack_part: bad rank");
+  const void* srcs[TV_MAX_RANKS] = {};
+  srcs[r] = src;
+  return repack_impl(srcs, p, r, u, ns, v, q, elem_bytes, dst, stream);
+}
+
+static int repack_impl(const void* const* srcs, int p, int only, int64_t u, int64_t ns, int64_t v, int64_t q,
+                       int elem_bytes, void* dst, void* stream) {
   using namespace tv;
   if (!srcs || p < 1 || p > TV_MAX_RANKS || u < 0 || ns < 0 || v < 0 || q < 1 ||
       (int64_t)(p - 1) * q >= ns + q || !(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8))
@@ -635,13 +680,37 @@ extern "C" int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, 
   if (!dst) return set_error(TV_EKERNEL, "tv_repack: null destination");
   Srcs s{};
   for (int r = 0; r < p; ++r) {
-    if (!srcs[r] && (int64_t)r * q < ns) return set_error(TV_EKERNEL, "tv_repack: null source");
+    if (!srcs[r] && (int64_t)r * q < ns && (only < 0 || only == r))
+      return set_error(TV_EKERNEL, "tv_repack: null source");
     s.p[r] = srcs[r];
   }
+  // 16-byte units throughout and short runs: a thread per unit
+  {
+    const int64_t qb = q * v * elem_bytes;
+    const int64_t lastn = ns - (int64_t)(p - 1) * q;
+    const int64_t lastb = lastn * v * elem_bytes;
+    const int64_t rowb = ns * v * elem_bytes;
+    uintptr_t al = reinterpret_cast<uintptr_t>(dst) | (uintptr_t)qb | (uintptr_t)(lastb > 0 ? lastb : 0) |
+                   (uintptr_t)rowb;
+    for (int r = 0; r < p; ++r)
+      if (only < 0 || only == r) al |= reinterpret_cast<uintptr_t>(srcs[r]);
+    const int64_t units = only < 0 ? u * rowb / 16 : u * (only == p - 1 ? lastb : qb) / 16;
+    if ((al & 15) == 0 && lastb > 0 && qb < 4096 && units < (int64_t)UINT32_MAX) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((units + 255) / 256, (int64_t)sms * 8));
+      k_repack_units<<<g, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+          s, p, only, (uint32_t)units, (uint32_t)(rowb / 16), (uint32_t)(qb / 16), (uint32_t)(lastb / 16),
+          static_cast<uint4*>(dst));
+      return launched("tv_repack");
+    }
+  }
+  // only >= 0: the runs of that one part (the others get no segments)
   RepackRuns runs{};
   for (int r = 0; r < p; ++r) {
     const int64_t lo = (int64_t)r * q;
-    const int64_t len = lo >= ns ? 0 : std::min(q, ns - lo) * v * elem_bytes;
+    const int64_t len = (lo >= ns || (only >= 0 && r != only)) ? 0 : std::min(q, ns - lo) * v * elem_bytes;
     runs.seg_before[r + 1] = runs.seg_before[r] + (len + kSeg - 1) / kSeg;
   }
   int dev = 0, sms = 148;
