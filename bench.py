@@ -108,6 +108,21 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
+    def wait_ready(self, timeout: float = 20.0) -> None:
+        """Block until nvidia-smi has written its first sample: its start-up
+        (NVML init on every GPU) stalled the launching ranks for milliseconds
+        when it overlapped a timed region (C3 at N = 4: 6.4 -> 16 ms steps)."""
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < timeout:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    return
+            except OSError:
+                return
+            if self.proc.poll() is not None:
+                return
+            time.sleep(0.02)
+
     def stop(self) -> dict | None:
         if self.proc is None:
             return None
@@ -355,14 +370,16 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
             return sweep_graph.replay()
         return tv.dtvc_sweep(dt, xs)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     clocks = ClockSampler() if rank == 0 else None
     if clocks:
         clocks.start()
+    for _ in range(args.warmup):
+        step()
+    if clocks:
+        clocks.wait_ready()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     lib = tv._lib.load()
     n_launch0 = lib.tv_launch_count()
@@ -628,6 +645,8 @@ def run_with_assembly(args, tv, dt, xs, s, world, job_bytes_step) -> dict:
         ms = float(t.item())
         out[strategy] = {"value": round(job_bytes_step / (ms / 1e3) / 1e9, 2), "unit": "GB/s",
                          "ms_per_step": round(ms, 4), "steps": n}
+        if strategy == "interleave":  # "multicast" (NVSwitch) or "push" (a store per peer)
+            out[strategy]["path"] = getattr(dt.group, "assembly_path", None)
     return out
 
 
@@ -766,13 +785,15 @@ def run_hopm(args, tv, wl, world, rank, key: str = "c4") -> dict | None:
     dt = tv.distribute_generated(shape, s, world, mode, fill="hash", seed=1, group=group)
     x0 = tv.initial_vectors(shape, mode)
     sweeps = args.steps
-    tv.dhopm3(dt, x0, sweeps=max(3, args.warmup))
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     clocks = ClockSampler() if rank == 0 else None
     if clocks:
         clocks.start()
+    tv.dhopm3(dt, x0, sweeps=max(3, args.warmup))
+    if clocks:
+        clocks.wait_ready()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     lib = tv._lib.load()
     n_launch0 = lib.tv_launch_count()

@@ -243,6 +243,13 @@ int tv_repack(const void* const* srcs, int p, int64_t u, int64_t ns, int64_t v, 
 int tv_repack_part(const void* src, int r, int p, int64_t u, int64_t ns, int64_t v, int64_t q, int elem_bytes,
                    void* dst, void* stream);
 
+/* tv_repack_part into EVERY rank's joint copy at once: dst_mc is the
+ * NVSwitch multicast address of the ranks' joint buffers (the same offset in
+ * each); each 16-byte unit is stored once (multimem.st) and replicated by
+ * the switch.  Needs 16-byte aligned buffers and runs (TV_EKERNEL else). */
+int tv_repack_part_multicast(const void* src, int r, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
+                             int elem_bytes, void* dst_mc, void* stream);
+
 /* Bytes at the start of a peer buffer reserved for the barrier words
  * (uint32 per rank); the transports put their data after it. */
 #define TV_PEER_HEADER 4096

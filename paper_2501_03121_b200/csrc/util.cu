@@ -390,6 +390,26 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The push of the interleave assembly through an NVSwitch multicast mapping:
+// every 16-byte unit of part `only` is stored ONCE to the multicast address
+// and the switch replicates it into every rank's joint copy (the unicast
+// push sends p - 1 copies over this GPU's links).  multimem.st moves bits:
+// the .f32 lanes are never interpreted.
+__global__ void __launch_bounds__(256)
+    k_repack_units_mc(const uint4* __restrict__ src, uint64_t total, uint64_t upr, uint64_t ext, uint64_t base,
+                      char* dst_mc) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const uint64_t i = t / ext;
+    const uint64_t off = t - i * ext;
+    const uint4 w = ld_stream16(src + t);
+    char* a = dst_mc + (i * upr + base + off) * 16;
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "r"(w.x), "r"(w.y),
+                 "r"(w.z), "r"(w.w)
+                 : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- fill ----
 __host__ __device__ inline uint64_t fill_hash(uint64_t seed, uint64_t g) {
   uint64_t z = (g + 1ULL) * 0x9E3779B97F4A7C15ULL + seed * 0xD1B54A32D192ED03ULL;
@@ -668,6 +688,29 @@ extern "C" int tv_repack_part(const void* src, int r, int p, int64_t u, int64_t 
   const void* srcs[TV_MAX_RANKS] = {};
   srcs[r] = src;
   return repack_impl(srcs, p, r, u, ns, v, q, elem_bytes, dst, stream);
+}
+
+extern "C" int tv_repack_part_multicast(const void* src, int r, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
+                                        int elem_bytes, void* dst_mc, void* stream) {
+  using namespace tv;
+  if (r < 0 || r >= p || p > TV_MAX_RANKS || u < 0 || ns < 0 || v < 0 || q < 1 || (int64_t)r * q >= ns ||
+      !(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8))
+    return set_error(TV_EKERNEL, "tv_repack_part_multicast: bad arguments");
+  if (u == 0 || v == 0) return TV_OK;
+  const int64_t extb = std::min(q, ns - (int64_t)r * q) * v * elem_bytes;
+  const int64_t qb = q * v * elem_bytes, rowb = ns * v * elem_bytes;
+  if (!src || !dst_mc || ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst_mc) |
+                           (uintptr_t)extb | (uintptr_t)qb | (uintptr_t)rowb) & 15))
+    return set_error(TV_EKERNEL, "tv_repack_part_multicast: needs 16-byte aligned runs and buffers");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t units = u * extb / 16;
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((units + 255) / 256, (int64_t)sms * 8));
+  k_repack_units_mc<<<g, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(src), (uint64_t)units, (uint64_t)(rowb / 16), (uint64_t)(extb / 16),
+      (uint64_t)(r * qb / 16), static_cast<char*>(dst_mc));
+  return launched("tv_repack_part_multicast");
 }
 
 static int repack_impl(const void* const* srcs, int p, int only, int64_t u, int64_t ns, int64_t v, int64_t q,

@@ -46,11 +46,14 @@ class PeerBuffer:
     address as mapped in this process.  Data starts TV_PEER_HEADER bytes in;
     the header holds the barrier words (zero on creation)."""
 
-    __slots__ = ("local", "bases", "capacity", "epoch", "bases_arr", "keep")
+    __slots__ = ("local", "bases", "capacity", "epoch", "bases_arr", "keep", "mc")
 
-    def __init__(self, local: torch.Tensor, bases: list[int], keep=None):
+    def __init__(self, local: torch.Tensor, bases: list[int], keep=None, mc: int = 0):
         self.local = local
         self.bases = [int(b) for b in bases]
+        # NVSwitch multicast address of the same bytes in every rank's buffer
+        # (a store there lands in all of them), 0 when the fabric has none
+        self.mc = int(mc)
         self.capacity = local.numel() - TV_PEER_HEADER
         self.epoch = 0
         self.bases_arr = (ctypes.c_void_p * len(self.bases))(*self.bases)
@@ -132,7 +135,14 @@ class TorchTransport:
         self._agree(err is None, device, "map", err)
         torch.cuda.synchronize(device)  # headers are zero before any peer posts
         self.barrier()
-        return PeerBuffer(t, [int(p) for p in hdl.buffer_ptrs], keep=hdl)
+        bases = [int(p) for p in hdl.buffer_ptrs]
+        mc = 0
+        try:  # only when the multicast mapping provably starts where our tensor does
+            if int(getattr(hdl, "offset", 0)) == 0 and bases[self.rank] == t.data_ptr():
+                mc = int(hdl.multicast_ptr or 0)
+        except Exception:  # noqa: BLE001 - no multicast object: unicast pushes
+            mc = 0
+        return PeerBuffer(t, bases, keep=hdl, mc=mc)
 
     def _agree(self, ok: bool, device, what: str, err) -> None:
         flag = torch.tensor([1 if ok else 0], dtype=torch.int32,

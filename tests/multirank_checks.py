@@ -169,6 +169,22 @@ def run_checks(rank: int, world: int, make_group, tv, O, *, quick: bool = False)
             x = O.demote((np.arange(ashape[0]) % 4) + 1.0, name).copy()
             got = tv.undistribute(tv.dtvc(dtf, x, 0), strategy).to_numpy()
             ok.append((name, "assemble-peer-out", strategy, _same(got, O.tvc(hosta.reshape(-1), ashape, x, 0, name))))
+        pb = getattr(fused, "_peer", None)
+        if pb is not None and pb.mc:  # 16-byte runs: one multicast store per unit, forced from 2 ranks on
+            from paper_2501_03121_b200 import comm as C
+
+            saved, C._MULTICAST_MIN = C._MULTICAST_MIN, 2
+            try:
+                for _ in range(2):
+                    got = tv.undistribute(dtf, "interleave").to_numpy()
+            finally:
+                C._MULTICAST_MIN = saved
+            ok.append((name, "assemble-multicast", fused.assembly_path == "multicast" and _same(got, hosta)))
+        # runs that are not 16-byte multiples take the per-peer push
+        oshape = (3, world * 3 - 1, 5)
+        hosto = O.demote(O.fill_values(oshape, "hash", seed=4), name).reshape(oshape)
+        dto = tv.distribute_generated(tv.Shape(oshape), 1, world, mode, fill="hash", seed=4, group=fused)
+        ok.append((name, "assemble-peer-ragged", _same(tv.undistribute(dto, "interleave").to_numpy(), hosto)))
         for k in (0, 3):
             x = O.demote((np.arange(ashape[k]) % 4) + 1.0, name).copy()
             got = tv.undistribute(tv.dtvc(dt, x, k)).to_numpy()
