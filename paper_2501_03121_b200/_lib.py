@@ -27,7 +27,7 @@ TV_PEER_HEADER = 4096
 TV_AR_NCCL, TV_AR_EXACT, TV_AR_MIXED = 0, 1, 2
 REGIMES = {0: "naive", 1: "rows", 2: "rows_short", 3: "cols", 4: "slabs", 5: "rows_u", 6: "cols_u",
            7: "slabs_u", 8: "staged", 9: "flat",
-           10: "flat_rows", 11: "staged_long", 12: "flat_u"}
+           10: "flat_rows", 11: "staged_long", 12: "flat_u", 13: "staged_tall"}
 
 _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p

@@ -22,7 +22,8 @@ enum {
   REG_FLAT = 9,      // narrow aligned slabs streamed as flat warp runs
   REG_FLAT_ROWS = 10,   // short aligned rows streamed as flat warp runs
   REG_STAGED_LONG = 11,  // larger unaligned slabs: row-run tiles by TMA, sums kept across tiles
-  REG_FLAT_U = 12        // tall narrow slabs of any row alignment: flat 16-byte runs, split-K
+  REG_FLAT_U = 12,       // tall narrow slabs of any row alignment: flat 16-byte runs, split-K
+  REG_STAGED_TALL = 13   // tall narrow unaligned slabs: TMA row tiles, split-K
 };
 
 // the five valid (storage, compute) pairs of precision.py:81-87

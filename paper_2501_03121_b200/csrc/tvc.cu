@@ -1179,6 +1179,132 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------- STAGED_TALL ----
+// Tall narrow slabs whose rows are not 16-byte multiples (n_k >= 1024 rows of
+// 2-31 elements, few slabs: [3000001, 7], [8, 1e6, 12] ...): the scalar
+// loads of SLABS_U put 2-8 bytes per lane in flight and ran latency-bound
+// at 0.8-2.7 TB/s.  Here a slab's rows are cut into chunks (split-K); a
+// persistent CTA walks the row tiles of its chunks in order, each tile ONE
+// TMA bulk copy of whole rows (aligned-down start, the buffer's ragged end by
+// scalar loads) on a two-stage mbarrier ring, as in STAGED_LONG; thread t sums
+// rows t, t + 256, ... of every tile into MAXV column accumulators (x read once
+// per row), and at chunk end the CTA folds them -- a fixed xor tree per warp,
+// then the 8 warps in order -- into the chunk's partial sums.
+template <int SD, typename C, int MAXV>
+__global__ void __launch_bounds__(kThreads)
+    k_staged_tall(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
+                  typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int v, int64_t nch, int64_t rpc,
+                  int tr, int sbytes, C alpha, C beta, int has_beta, C* __restrict__ ws) {
+  PdlScope pdl_scope;
+  using T = typename St<SD>::T;
+  constexpr int SB = sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int stride_b = sbytes + 32;
+  unsigned char* const stage0 = smem_raw;
+  C* red = reinterpret_cast<C*>(smem_raw + 2 * stride_b);  // [kWarps][MAXV]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 2 * stride_b + (kWarps * MAXV * sizeof(C) + 7) / 8 * 8);
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const unsigned char* gbase = reinterpret_cast<const unsigned char*>(A);
+  const int64_t row_bytes = (int64_t)v * SB;
+  const int64_t total_bytes = u * nk * row_bytes;
+  const int64_t bulk_end = total_bytes & ~(int64_t)15;
+  const int64_t units = u * nch;
+  // cursors (unit, first row j0 of the tile); a unit is (slab unit / nch,
+  // rows [(unit % nch) * rpc, +rpc) clipped to nk)
+  auto unit_end = [&](int64_t unit) {
+    const int64_t e = (unit % nch + 1) * rpc;
+    return e < nk ? e : nk;
+  };
+  int64_t f_unit = blockIdx.x, f_j0 = (f_unit % nch) * rpc;  // fetch cursor (thread 0)
+  auto fetch = [&](int k) {
+    const int64_t je = unit_end(f_unit);
+    const int64_t j1 = f_j0 + tr < je ? f_j0 + tr : je;
+    const int64_t b0 = ((f_unit / nch) * nk + f_j0) * row_bytes;
+    const int64_t a0 = b0 & ~(int64_t)15;
+    const int64_t e16 = (b0 + (j1 - f_j0) * row_bytes + 15) & ~(int64_t)15;
+    const int64_t a1 = e16 < bulk_end ? e16 : bulk_end;
+    const unsigned nb = a1 > a0 ? (unsigned)(a1 - a0) : 0u;
+    mbar_expect_tx(&bars[k], nb);
+    if (nb) bulk_g2s(stage0 + k * stride_b, gbase + a0, nb, &bars[k]);
+    if (j1 == je) {
+      f_unit += gridDim.x;
+      f_j0 = (f_unit % nch) * rpc;
+    } else {
+      f_j0 = j1;
+    }
+  };
+  if (threadIdx.x == 0 && blockIdx.x < units) fetch(0);
+
+  C acc[MAXV];
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) acc[m] = C(0);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t unit = blockIdx.x, j0 = (unit % nch) * rpc;
+  for (int64_t t = 0; unit < units; ++t) {
+    const int k = (int)(t & 1);
+    const int64_t je = unit_end(unit);
+    const int64_t j1 = j0 + tr < je ? j0 + tr : je;
+    if (threadIdx.x == 0 && (j1 < je || unit + gridDim.x < units)) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      fetch(k ^ 1);
+    }
+    const int64_t slab = unit / nch;
+    const int64_t b0 = (slab * nk + j0) * row_bytes;
+    unsigned char* const sp = stage0 + k * stride_b;
+    mbar_wait(&bars[k], (unsigned)(t >> 1) & 1u);
+    if (b0 + (j1 - j0) * row_bytes > bulk_end) {  // block-uniform: the buffer's ragged end
+      const int64_t a0 = b0 & ~(int64_t)15;
+      for (int64_t b = (bulk_end > a0 ? bulk_end : a0) + threadIdx.x; b < total_bytes; b += blockDim.x)
+        sp[b - a0] = gbase[b];
+      __syncthreads();
+    }
+    const T* tile = reinterpret_cast<const T*>(sp + (b0 & 15));
+    const int rows = (int)(j1 - j0);
+    for (int r = threadIdx.x; r < rows; r += kThreads) {
+      const C xj = promote<SD, C>(__ldg(x + j0 + r));
+      const T* rp = tile + r * v;
+#pragma unroll
+      for (int m = 0; m < MAXV; ++m)
+        if (m < v) acc[m] = fma(promote<SD, C>(rp[m]), xj, acc[m]);
+    }
+    if (j1 == je) {  // chunk done: fold the CTA's row sums, column by column
+#pragma unroll
+      for (int m = 0; m < MAXV; ++m) {
+        if (m < v) {
+          C s = acc[m];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+          if (lane == 0) red[w * MAXV + m] = s;
+        }
+        acc[m] = C(0);
+      }
+      __syncthreads();
+      if (threadIdx.x < v) {
+        C s = red[threadIdx.x];
+#pragma unroll
+        for (int ww = 1; ww < kWarps; ++ww) s += red[ww * MAXV + threadIdx.x];
+        if (ws != nullptr) {
+          ws[unit * v + threadIdx.x] = s;
+        } else {
+          const int64_t o = slab * v + threadIdx.x;
+          y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
+        }
+      }
+      unit += gridDim.x;
+      j0 = (unit % nch) * rpc;
+    } else {
+      j0 = j1;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------- TVC + NORMALIZE ----
 // The last contraction of a dHOPM3 iteration (the carried 2-mode tensor
 // contracted to the iteration's vector, hopm.py:295-319) with the vector
@@ -1442,6 +1568,8 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
   // alignment whose group period is supported
   const bool flat_u_ok = base_al && contiguous && su_al && v > 1 && flat_u_period(v, VEC) > 0 &&
                          (int64_t)kWarps * 32 * flat_u_period(v, VEC) * VEC * 8 <= 96 * 1024;
+  // STAGED_TALL: contiguous narrow slabs (2-31 elements) from a 16-byte base
+  const bool tall_ok = base_al && contiguous && v > 1 && v < 32 && v * sb <= stb;
   // a forced regime the view cannot take falls through to the heuristics
   const int forced = forced_regime();
   if (forced > 0) {
@@ -1452,6 +1580,7 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
                     (forced == REG_COLS_U && v > 1) || (forced == REG_SLABS_U && v > 1 && v < 32) ||
                     (forced == REG_STAGED && stageable) || (forced == REG_FLAT && flat_ok) ||
                     (forced == REG_FLAT_ROWS && flat_rows_ok) || (forced == REG_FLAT_U && flat_u_ok) ||
+                    (forced == REG_STAGED_TALL && tall_ok) ||
                     (forced == REG_STAGED_LONG && base_al && contiguous && v > 1 && v <= kLongCols &&
                      v * sb <= stb && u > 1 && nk * 8 <= 96 * 1024);
     if (ok) return forced;
@@ -1475,6 +1604,11 @@ static int regime_strided(const void* A, int sb, int64_t u, int64_t nk, int64_t 
     // narrow rows: [8, 1e6, 12] bf16 1.02 -> 2.32 TB/s); for 4- and 8-byte
     // storage and aligned rows SLABS / SLABS_U measured as fast or faster
     // (profiles/r02_flat_u_ab/)
+    static const int st_env = [] {  // TENVEC_B200_STAGED_TALL=0: the previous choice, for A/B runs
+      const char* e = getenv("TENVEC_B200_STAGED_TALL");
+      return e ? atoi(e) : 1;
+    }();
+    if (tall_ok && st_env != 0 && !al_cols) return REG_STAGED_TALL;
     if (flat_u_ok && fu_env != 0 && sb == 2 && !al_cols) return REG_FLAT_U;
     return al_cols ? REG_SLABS : REG_SLABS_U;
   }
@@ -1591,6 +1725,39 @@ static void launch_rows_auto(const void* A, const void* x, void* y, int64_t u, i
 // cut into nch chunks, each chunk's partial sums go to a workspace in the
 // compute type, and k_split_fold adds the chunks of every output in chunk
 // order (deterministic) and applies the epilogue.
+template <int SD, typename C>
+__global__ void __launch_bounds__(256)
+    k_split_fold_cta(const C* __restrict__ ws, int64_t nch, int64_t n, int64_t v,
+                     typename St<SD>::T* __restrict__ y, C alpha, C beta, int has_beta) {
+  // few outputs, thousands of chunks: a CTA per output, thread t sums chunks
+  // t, t + 256, ... in order (loads 4 deep), then a fixed pairwise tree
+  __shared__ C red[256];
+  const int t = threadIdx.x;
+  for (int64_t o = blockIdx.x; o < n; o += gridDim.x) {
+    const int64_t i = o / v;
+    const C* p = ws + i * nch * v + (o - i * v);
+    C s = C(0);
+    int64_t ch = t;
+    for (; ch + 3 * 256 < nch; ch += 4 * 256) {
+      C b[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) b[k] = p[(ch + k * 256) * v];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s += b[k];
+    }
+    for (; ch < nch; ch += 256) s += p[ch * v];
+    red[t] = s;
+    __syncthreads();
+#pragma unroll
+    for (int h = 128; h > 0; h >>= 1) {
+      if (t < h) red[t] += red[t + h];
+      __syncthreads();
+    }
+    if (t == 0) y[o] = epilogue<SD, C>(red[0], alpha, beta, has_beta != 0, y + o);
+    __syncthreads();
+  }
+}
+
 template <int SD, typename C, bool WARP>
 __global__ void __launch_bounds__(256)
     k_split_fold(const C* __restrict__ ws, int64_t nch, int64_t n, int64_t v,
@@ -1604,7 +1771,18 @@ __global__ void __launch_bounds__(256)
       const int64_t i = o / v;
       const C* p = ws + i * nch * v + (o - i * v);
       C s = C(0);
-      for (int64_t ch = lane; ch < nch; ch += 32) s += p[ch * v];
+      // loads batched 8 deep (the adds keep their order): a few outputs of
+      // thousands of chunks were a chain of dependent loads (4 M x 8 fp64:
+      // 63 us for the fold vs 53 us for the contraction)
+      int64_t ch = lane;
+      for (; ch + 7 * 32 < nch; ch += 8 * 32) {
+        C b[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) b[t] = p[(ch + t * 32) * v];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) s += b[t];
+      }
+      for (; ch < nch; ch += 32) s += p[ch * v];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       if (lane == 0) y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
@@ -1614,7 +1792,15 @@ __global__ void __launch_bounds__(256)
       const int64_t i = o / v;
       const C* p = ws + i * nch * v + (o - i * v);
       C s = p[0];
-      for (int64_t ch = 1; ch < nch; ++ch) s += p[ch * v];
+      int64_t ch = 1;
+      for (; ch + 7 < nch; ch += 8) {
+        C b[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) b[t] = p[(ch + t) * v];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) s += b[t];
+      }
+      for (; ch < nch; ++ch) s += p[ch * v];
       y[o] = epilogue<SD, C>(s, alpha, beta, has_beta != 0, y + o);
     }
   }
@@ -1639,8 +1825,13 @@ static int64_t cols_split(int64_t blocks, int64_t nk) {
 }
 
 static int64_t slabs_split(int64_t u, int64_t nk) {
+  static const int64_t per_sm = [] {  // TENVEC_B200_SLAB_SPLIT: warp units per SM, for A/B runs
+    const char* e = getenv("TENVEC_B200_SLAB_SPLIT");
+    const int r = e ? atoi(e) : 32;
+    return (int64_t)(r < 8 ? 8 : (r > 256 ? 256 : r));
+  }();
   if (!(u < 32LL * sm_count() && nk >= 256)) return 1;
-  const int64_t nch = std::min<int64_t>(cdiv(32LL * sm_count(), u), nk / 64);
+  const int64_t nch = std::min<int64_t>(cdiv(per_sm * sm_count(), u), nk / 64);
   return nch > 1 ? cdiv(nk, cdiv(nk, nch)) : 1;
 }
 
@@ -1669,7 +1860,10 @@ static void split_finish(C* ws, const Ws& given, int64_t nch, int64_t u, int64_t
                          int hb, cudaStream_t st) {
   using T = typename St<SD>::T;
   const int64_t n = u * v;
-  if (nch >= 32) {
+  if (nch >= 1024 && n <= 2LL * sm_count()) {
+    count_launch();
+    k_split_fold_cta<SD, C><<<(unsigned)n, 256, 0, st>>>(ws, nch, n, v, (T*)y, al, be, hb);
+  } else if (nch >= 32) {
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 8LL * sm_count()));
     count_launch();
     k_split_fold<SD, C, true><<<g, 256, 0, st>>>(ws, nch, n, v, (T*)y, al, be, hb);
@@ -1757,6 +1951,45 @@ static void launch_staged_long(const void* A, const void* x, void* y, int64_t u,
   else go(k_staged_long<SD, C, 16>);
 }
 
+// STAGED_TALL geometry: rows per tile, chunks per slab and rows per chunk
+// (a pure function of the view, so tv_tvc_workspace_bytes can size it)
+static void staged_tall_split(int64_t u, int64_t nk, int64_t v, int sb, int* tr, int64_t* nch, int64_t* rpc) {
+  const int64_t rmax = std::max<int64_t>(1, stage_bytes() / (v * sb));
+  const int64_t want = cdiv(8LL * sm_count(), u);  // ~4 chunks per co-resident CTA
+  int64_t n = std::max<int64_t>(1, std::min<int64_t>(want, cdiv(nk, rmax)));
+  const int64_t r = cdiv(nk, n);
+  *tr = (int)std::min<int64_t>(rmax, r);
+  *rpc = r;
+  *nch = cdiv(nk, r);
+}
+
+template <int SD, typename C>
+static int launch_staged_tall(const void* A, const void* x, void* y, int64_t u, int64_t nk, int64_t v, C al,
+                              C be, int hb, const Ws& wsa, cudaStream_t st) {
+  using T = typename St<SD>::T;
+  int tr = 1;
+  int64_t nch = 1, rpc = nk;
+  staged_tall_split(u, nk, v, (int)sizeof(T), &tr, &nch, &rpc);
+  int rc = TV_OK;
+  C* ws = nullptr;
+  if (nch > 1 && (ws = split_ws<C>(wsa, u * nch * v, st, &rc)) == nullptr) return rc;
+  const int sbytes = stage_bytes();
+  const int maxv = v <= 8 ? 8 : (v <= 16 ? 16 : 32);
+  const size_t smem = 2 * (size_t)(sbytes + 32) + ((size_t)kWarps * maxv * sizeof(C) + 7) / 8 * 8 +
+                      2 * sizeof(uint64_t);
+  const unsigned grid = (unsigned)std::min<int64_t>(u * nch, 2LL * sm_count());
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_k(kern, grid, kThreads, smem, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v, nch, rpc, tr,
+             sbytes, al, be, hb, ws);
+  };
+  if (maxv == 8) go(k_staged_tall<SD, C, 8>);
+  else if (maxv == 16) go(k_staged_tall<SD, C, 16>);
+  else go(k_staged_tall<SD, C, 32>);
+  if (ws != nullptr) split_finish<SD, C>(ws, wsa, nch, u, v, y, al, be, hb, st);
+  return TV_OK;
+}
+
 // column blocks of a COLS launch (row phases JR from the view)
 template <int SD, bool AL>
 static int64_t cols_blocks(int64_t u, int64_t nk, int64_t v, int* jr_out, int64_t* ntile_out) {
@@ -1837,6 +2070,12 @@ static int64_t ws_bytes_typed(const void* A, int64_t u, int64_t nk, int64_t v, i
       flat_u_split(u, nk, v, (int)VecN<SD>::N, flat_u_period(v, (int)VecN<SD>::N), &nch, &rpc);
       break;
     }
+    case REG_STAGED_TALL: {
+      int tr = 1;
+      int64_t rpc = nk;
+      staged_tall_split(u, nk, v, (int)sizeof(T), &tr, &nch, &rpc);
+      break;
+    }
     default: break;
   }
   return nch > 1 ? u * nch * v * (int64_t)sizeof(C) : 0;
@@ -1865,6 +2104,9 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       break;
     case REG_STAGED_LONG:
       launch_staged_long<SD, C>(A, x, y, u, nk, v, al, be, hb, st);
+      break;
+    case REG_STAGED_TALL:
+      rc = launch_staged_tall<SD, C>(A, x, y, u, nk, v, al, be, hb, wsa, st);
       break;
     case REG_ROWS_SHORT: {
       constexpr int UNR = 4;
@@ -1947,12 +2189,25 @@ static int tvc_typed(const void* A, int64_t u, int64_t nk, int64_t v, int64_t su
       if (nch > 1 && (ws = split_ws<C>(wsa, u * nch * v, st, &rc)) == nullptr) return rc;
       const int64_t rpc = cdiv(nk, nch);
       const unsigned grid = grid_for(u * nch, kWarps, 32);
-      if (reg == REG_SLABS)
-        launch_k(k_slabs<SD, C, 4, true>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
-                                                           su, sk, al, be, hb, nch, rpc, ws);
-      else
-        launch_k(k_slabs<SD, C, 8, false>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
-                                                            su, sk, al, be, hb, nch, rpc, ws);
+      static const int unr_env = [] {  // TENVEC_B200_SLAB_UNR=2: twice the batch depth, for A/B runs
+        const char* e = getenv("TENVEC_B200_SLAB_UNR");
+        return e ? atoi(e) : 1;
+      }();
+      if (reg == REG_SLABS) {
+        if (unr_env == 2)
+          launch_k(k_slabs<SD, C, 8, true>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
+                   su, sk, al, be, hb, nch, rpc, ws);
+        else
+          launch_k(k_slabs<SD, C, 4, true>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v,
+                   su, sk, al, be, hb, nch, rpc, ws);
+      } else {
+        if (unr_env == 2)
+          launch_k(k_slabs<SD, C, 16, false>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk,
+                   (int)v, su, sk, al, be, hb, nch, rpc, ws);
+        else
+          launch_k(k_slabs<SD, C, 8, false>, grid, kThreads, 0, st, (const T*)A, (const T*)x, (T*)y, u, nk,
+                   (int)v, su, sk, al, be, hb, nch, rpc, ws);
+      }
       if (ws != nullptr) split_finish<SD, C>(ws, wsa, nch, u, v, y, al, be, hb, st);
       break;
     }

@@ -138,6 +138,11 @@ REGIME_CASES = [
     ((3, 2048, 24), 1, "flat_u"),
     ((5000, 16), 0, "flat_u"),
     ((1, 1100, 3), 1, "flat_u"),
+    ((2, 3000, 6), 1, "staged_tall"),
+    ((1, 1100, 3), 1, "staged_tall"),
+    ((3, 5000, 31), 1, "staged_tall"),
+    ((5001, 5), 0, "staged_tall"),  # integer sums stay below 2^24 in f32
+    ((2, 4000, 12), 1, "staged_tall"),
 ]
 
 
@@ -147,8 +152,9 @@ NATURAL = {((300, 96), 1): "staged", ((96, 96, 12), 2): "staged", ((700, 20), 1)
            ((4, 300, 21), 1): "staged", ((61, 130, 1), 1): "staged", ((77, 330), 1): "staged",
            ((7, 40, 363), 1): "cols_u", ((5, 41, 363), 1): "cols_u", ((9, 300, 50), 1): "cols_u",
            ((3, 5, 4000), 1): "cols", ((2, 700, 33), 1): "cols_u", ((96, 96, 12), 1): "staged",
-           ((3, 200, 20), 1): "staged", ((4000, 12), 0): "slabs", ((2, 3000, 6), 1): "slabs_u",
-           ((3, 2048, 24), 1): "slabs", ((5000, 16), 0): "slabs", ((1, 1100, 3), 1): "slabs_u"}
+           ((3, 200, 20), 1): "staged", ((4000, 12), 0): "slabs", ((2, 3000, 6), 1): "staged_tall",
+           ((3, 2048, 24), 1): "slabs", ((5000, 16), 0): "slabs", ((1, 1100, 3), 1): "staged_tall",
+           ((2, 4000, 12), 1): "slabs"}
 
 
 @pytest.fixture
@@ -321,8 +327,9 @@ def test_large_views_sampled_exact(tv, mode_name, shape):
 
 
 TALL = [((300_000, 8), 0, "slabs"), ((1, 200_000, 16), 1, "slabs"), ((100_000, 160), 0, "cols"),
-        ((40_001, 301), 0, "cols_u"), ((1, 3_000_000), 1, "slabs_u"), ((3, 100_001, 7), 1, "slabs_u"),
-        ((2, 50_000, 24), 1, "slabs"), ((70_000, 2), 0, "slabs_u"), ((1_000_003, 12), 0, "slabs"),
+        ((40_001, 301), 0, "cols_u"), ((1, 3_000_000), 1, "slabs_u"), ((3, 100_001, 7), 1, "staged_tall"),
+        ((2, 50_000, 24), 1, "slabs"), ((70_000, 2), 0, "staged_tall"), ((1_000_003, 12), 0, "slabs"),
+        ((3_000_001, 7), 0, "staged_tall"), ((2, 400_000, 31), 1, "staged_tall"),
         ((8, 200_000, 12), 1, "slabs")]
 
 

@@ -195,9 +195,9 @@ def test_library_argument_validation_without_gpu():
     assert lib.tv_tvc_regime(p, 0, 100000, 10, 1000) == 11  # aligned short columns -> row-run tiles
     assert lib.tv_tvc_regime(p, 0, 2048, 2048, 4096) == 3  # aligned long columns stay COLS
     assert lib.tv_tvc_regime(p, 0, 979, 979, 979) == 6     # too few slabs to balance -> scalar columns
-    assert lib.tv_tvc_regime(p, 3, 8, 1000000, 12) == 12   # tall unaligned bf16 slabs -> flat runs
+    assert lib.tv_tvc_regime(p, 3, 8, 1000000, 12) == 13   # tall unaligned bf16 slabs -> row tiles
     assert lib.tv_tvc_regime(p, 1, 8, 1000000, 12) == 4    # the same in fp32 (aligned) -> slabs
-    assert lib.tv_tvc_regime(p, 0, 1, 3000001, 7) == 7     # tall unaligned fp64 -> scalar slabs
+    assert lib.tv_tvc_regime(p, 0, 1, 3000001, 7) == 13    # tall unaligned fp64 -> row tiles
     # the diagnostic override pins a regime only where the view can take it
     prev = lib.tv_set_regime_override(1)
     try:
