@@ -28,8 +28,12 @@
 //               mbarriers, double-buffered), dot products from shared memory.
 //   STAGED_LONG larger slabs of <= 4096 columns: row-run tiles, one bulk copy
 //               each, column sums kept in registers across a slab's tiles.
-//   split-K     few outputs, long columns (COLS / SLABS): row chunks write
-//               partial sums to a workspace folded in chunk order.
+//   STAGED_TALL tall narrow unaligned slabs (n_k >= 1024 rows of 2-31
+//               elements, few slabs): split-K row chunks, each a run of TMA
+//               row tiles; a thread sums whole rows into column registers.
+//   split-K     few outputs, long columns (COLS / SLABS / FLAT_U /
+//               STAGED_TALL): row chunks write partial sums to a workspace
+//               folded in chunk order.
 //
 // Every regime has an aligned form (one 16-byte ld.global.nc.L1::no_allocate
 // per lane, "unit" = 16 bytes) and an unaligned form for rows or slabs that do
