@@ -1194,8 +1194,10 @@ __global__ void __launch_bounds__(kThreads)
 // rows t, t + 256, ... of every tile into MAXV column accumulators (x read once
 // per row), and at chunk end the CTA folds them -- a fixed xor tree per warp,
 // then the 8 warps in order -- into the chunk's partial sums.
+constexpr int kTallRowsPerThread = 16;  // rows per tile <= 16 * kThreads
+
 template <int SD, typename C, int MAXV>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
     k_staged_tall(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
                   typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int v, int64_t nch, int64_t rpc,
                   int tr, int sbytes, C alpha, C beta, int has_beta, C* __restrict__ ws) {
@@ -1203,15 +1205,19 @@ __global__ void __launch_bounds__(kThreads)
   using T = typename St<SD>::T;
   constexpr int SB = sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int stride_b = sbytes + 32;
+  const int stride_b = sbytes + 32 + (MAXV * SB + 15) / 16 * 16;
   unsigned char* const stage0 = smem_raw;
   C* red = reinterpret_cast<C*>(smem_raw + 2 * stride_b);  // [kWarps][MAXV]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 2 * stride_b + (kWarps * MAXV * sizeof(C) + 7) / 8 * 8);
+  // the last row's over-read (columns past v) never sees uninitialised bytes
+  for (int i = threadIdx.x; i < 2 * stride_b / 16; i += kThreads)
+    reinterpret_cast<uint4*>(stage0)[i] = make_uint4(0u, 0u, 0u, 0u);
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   __syncthreads();
 
   const unsigned char* gbase = reinterpret_cast<const unsigned char*>(A);
@@ -1270,12 +1276,41 @@ __global__ void __launch_bounds__(kThreads)
     }
     const T* tile = reinterpret_cast<const T*>(sp + (b0 & 15));
     const int rows = (int)(j1 - j0);
-    for (int r = threadIdx.x; r < rows; r += kThreads) {
-      const C xj = promote<SD, C>(__ldg(x + j0 + r));
-      const T* rp = tile + r * v;
+    // x of this thread's rows first (independent loads, one latency per
+    // tile), then MAXV columns per row with no predicates: the columns past v
+    // read the next row's elements (or the stage's zero pad) into
+    // accumulators that are never folded
+    C xr[kTallRowsPerThread];
 #pragma unroll
-      for (int m = 0; m < MAXV; ++m)
-        if (m < v) acc[m] = fma(promote<SD, C>(rp[m]), xj, acc[m]);
+    for (int i = 0; i < kTallRowsPerThread; ++i) {
+      const int r = threadIdx.x + i * kThreads;
+      xr[i] = r < rows ? promote<SD, C>(__ldg(x + j0 + r)) : C(0);
+    }
+#pragma unroll
+    for (int i = 0; i < kTallRowsPerThread; ++i) {
+      const int r = threadIdx.x + i * kThreads;
+      if (r < rows) {
+        if constexpr (SB == 2) {
+          // 2-byte elements: the row as 32-bit words from the stage base,
+          // re-paired by a funnel shift when it starts on an odd element
+          const int e0 = (int)((b0 & 15) >> 1) + r * v;
+          const uint32_t* wp = reinterpret_cast<const uint32_t*>(sp) + (e0 >> 1);
+          const unsigned sh = (unsigned)(e0 & 1) * 16u;
+          uint32_t wv[MAXV / 2 + 1];
+#pragma unroll
+          for (int q = 0; q <= MAXV / 2; ++q) wv[q] = wp[q];
+#pragma unroll
+          for (int q = 0; q < MAXV / 2; ++q) {
+            const uint32_t pr = __funnelshift_r(wv[q], wv[q + 1], sh);
+            acc[2 * q] = fma(promote<SD, C>((T)(pr & 0xffffu)), xr[i], acc[2 * q]);
+            acc[2 * q + 1] = fma(promote<SD, C>((T)(pr >> 16)), xr[i], acc[2 * q + 1]);
+          }
+        } else {
+          const T* rp = tile + r * v;
+#pragma unroll
+          for (int m = 0; m < MAXV; ++m) acc[m] = fma(promote<SD, C>(rp[m]), xr[i], acc[m]);
+        }
+      }
     }
     if (j1 == je) {  // chunk done: fold the CTA's row sums, column by column
 #pragma unroll
@@ -1958,7 +1993,7 @@ static void launch_staged_long(const void* A, const void* x, void* y, int64_t u,
 // STAGED_TALL geometry: rows per tile, chunks per slab and rows per chunk
 // (a pure function of the view, so tv_tvc_workspace_bytes can size it)
 static void staged_tall_split(int64_t u, int64_t nk, int64_t v, int sb, int* tr, int64_t* nch, int64_t* rpc) {
-  const int64_t rmax = std::max<int64_t>(1, stage_bytes() / (v * sb));
+  const int64_t rmax = std::max<int64_t>(1, std::min<int64_t>(stage_bytes() / (v * sb), 16LL * kThreads));
   const int64_t want = cdiv(8LL * sm_count(), u);  // ~4 chunks per co-resident CTA
   int64_t n = std::max<int64_t>(1, std::min<int64_t>(want, cdiv(nk, rmax)));
   const int64_t r = cdiv(nk, n);
@@ -1978,18 +2013,23 @@ static int launch_staged_tall(const void* A, const void* x, void* y, int64_t u, 
   C* ws = nullptr;
   if (nch > 1 && (ws = split_ws<C>(wsa, u * nch * v, st, &rc)) == nullptr) return rc;
   const int sbytes = stage_bytes();
-  const int maxv = v <= 8 ? 8 : (v <= 16 ? 16 : 32);
-  const size_t smem = 2 * (size_t)(sbytes + 32) + ((size_t)kWarps * maxv * sizeof(C) + 7) / 8 * 8 +
-                      2 * sizeof(uint64_t);
+  const int maxv = v <= 4 ? 4 : v <= 8 ? 8 : v <= 12 ? 12 : v <= 16 ? 16 : v <= 24 ? 24 : 32;
+  const size_t stride_b = (size_t)sbytes + 32 + ((size_t)maxv * sizeof(T) + 15) / 16 * 16;
+  const size_t smem = 2 * stride_b + ((size_t)kWarps * maxv * sizeof(C) + 7) / 8 * 8 + 2 * sizeof(uint64_t);
   const unsigned grid = (unsigned)std::min<int64_t>(u * nch, 2LL * sm_count());
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_k(kern, grid, kThreads, smem, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v, nch, rpc, tr,
              sbytes, al, be, hb, ws);
   };
-  if (maxv == 8) go(k_staged_tall<SD, C, 8>);
-  else if (maxv == 16) go(k_staged_tall<SD, C, 16>);
-  else go(k_staged_tall<SD, C, 32>);
+  switch (maxv) {
+    case 4: go(k_staged_tall<SD, C, 4>); break;
+    case 8: go(k_staged_tall<SD, C, 8>); break;
+    case 12: go(k_staged_tall<SD, C, 12>); break;
+    case 16: go(k_staged_tall<SD, C, 16>); break;
+    case 24: go(k_staged_tall<SD, C, 24>); break;
+    default: go(k_staged_tall<SD, C, 32>); break;
+  }
   if (ws != nullptr) split_finish<SD, C>(ws, wsa, nch, u, v, y, al, be, hb, st);
   return TV_OK;
 }
