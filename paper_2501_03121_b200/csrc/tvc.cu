@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads)
 // rows j = r, r + JR, ... of its stripe.  Aligned: lane owns one 16-byte
 // vector (VEC adjacent columns); unaligned: lane owns VEC columns 32 apart, so
 // each of its scalar loads is part of one contiguous 32-element warp access.
-template <int SD, typename C, int JR, int UNR, bool AL, bool SPLIT = false>
+template <int SD, typename C, int JR, int UNR, bool AL, bool SPLIT = false, bool DB = false>
 __global__ void __launch_bounds__(kThreads)
     k_cols(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
            typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk_all, int64_t v, int64_t su,
@@ -424,6 +424,45 @@ __global__ void __launch_bounds__(kThreads)
       bool ok[VEC];
 #pragma unroll
       for (int e = 0; e < VEC; ++e) ok[e] = col_of(e) < v;
+      if constexpr (DB) {
+        // long columns of few stripes (paper d = 2 k = 0: 3.2 CTAs per SM):
+        // a register double buffer keeps batch b + 1 in flight while batch
+        // b folds -- twice the bytes in flight per warp
+        const T* cb = base + sbase * VEC + lane;
+        const int64_t step = (int64_t)JR * UNR;
+        auto ldb = [&](T (&b)[UNR][VEC], int64_t jj) {
+#pragma unroll
+          for (int t = 0; t < UNR; ++t)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+              if (ok[e]) b[t][e] = ld_stream_elem(cb + (jj + (int64_t)t * JR) * sk + e * 32);
+        };
+        auto fld = [&](const T (&b)[UNR][VEC], int64_t jj) {
+#pragma unroll
+          for (int t = 0; t < UNR; ++t) {
+            const C xj = promote<SD, C>(__ldg(x + jj + (int64_t)t * JR));
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+              if (ok[e]) acc[e] = fma(promote<SD, C>(b[t][e]), xj, acc[e]);
+          }
+        };
+        if (j0 + (int64_t)(UNR - 1) * JR < nk) {
+          T cur[UNR][VEC], nxt[UNR][VEC];
+          ldb(cur, j0);
+          for (;;) {
+            const int64_t jn = j0 + step;
+            const bool more = jn + (int64_t)(UNR - 1) * JR < nk;
+            if (more) ldb(nxt, jn);
+            fld(cur, j0);
+            j0 = jn;
+            if (!more) break;
+#pragma unroll
+            for (int t = 0; t < UNR; ++t)
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) cur[t][e] = nxt[t][e];
+          }
+        }
+      }
       for (; j0 < nk; j0 += (int64_t)JR * UNR) {
         T buf[UNR][VEC];
 #pragma unroll
@@ -2090,6 +2129,12 @@ static int launch_cols(const void* A, const void* x, void* y, int64_t u, int64_t
       return sp ? go(k_cols<SD, C, 4, 3, false, true>) : go(k_cols<SD, C, 4, 3, false, false>);
     return go(k_cols<SD, C, 1, 3, false, true>);
   }
+  static const int db_env = [] {  // TENVEC_B200_COLS_U_DB=0: single-buffered COLS_U, for A/B runs
+    const char* e = getenv("TENVEC_B200_COLS_U_DB");
+    return e ? atoi(e) : 1;
+  }();
+  if (!AL && JR == 8 && db_env != 0)
+    return sp ? go(k_cols<SD, C, 8, UA_UNR, false, true, true>) : go(k_cols<SD, C, 8, UA_UNR, false, false, true>);
   switch (JR) {
     case 1: return (sp || !AL) ? go(k_cols<SD, C, 1, AL ? 8 : UA_UNR, AL, true>) : go(k_cols<SD, C, 1, AL ? 8 : UA_UNR, AL, false>);
     case 2: return sp ? go(k_cols<SD, C, 2, AL ? 8 : UA_UNR, AL, true>) : go(k_cols<SD, C, 2, AL ? 8 : UA_UNR, AL, false>);

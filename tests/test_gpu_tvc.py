@@ -143,6 +143,8 @@ REGIME_CASES = [
     ((3, 5000, 31), 1, "staged_tall"),
     ((5001, 5), 0, "staged_tall"),  # integer sums stay below 2^24 in f32
     ((2, 4000, 12), 1, "staged_tall"),
+    ((2, 1200, 77), 1, "cols_u"),  # 8 row phases: the double-buffered COLS_U
+    ((1300, 333), 0, "cols_u"),
 ]
 
 
