@@ -86,6 +86,9 @@ def _traffic(workload: str, kernel: str, world: int = 1):
         return None
 
 
+# device-side hold before a timed loop (~0.5 s at B200 clocks)
+HOLD_CYCLES = 1_000_000_000
+
 # -- clocks -------------------------------------------------------------------
 
 CLOCK_Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -384,6 +387,11 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
     lib = tv._lib.load()
     n_launch0 = lib.tv_launch_count()
     last = None
+    # hold the stream ~0.5 s (outside every timed event pair) while the host
+    # enqueues all K steps: a host stall during the loop (an nvidia-smi query
+    # holding the driver lock cost one step 180 ms, profiles/r02_bench_variance/)
+    # then cannot leave the GPU idle inside a timed step
+    _block_stream(torch, HOLD_CYCLES)
     for i in range(args.steps):
         if flush is not None:
             flush()
@@ -455,6 +463,7 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
+        "step_ms_rank0": [round(x, 3) for x in step_ms],
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
@@ -635,6 +644,7 @@ def run_with_assembly(args, tv, dt, xs, s, world, job_bytes_step) -> dict:
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n = max(3, min(args.steps, 10))
+        _block_stream(torch, HOLD_CYCLES)
         e0.record()
         for _ in range(n):
             astep()
@@ -797,6 +807,7 @@ def run_hopm(args, tv, wl, world, rank, key: str = "c4") -> dict | None:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     lib = tv._lib.load()
     n_launch0 = lib.tv_launch_count()
+    _block_stream(torch, HOLD_CYCLES)  # the host enqueues ahead (see run_sweep)
     e0.record()
     res = tv.dhopm3(dt, x0, sweeps=sweeps)
     e1.record()

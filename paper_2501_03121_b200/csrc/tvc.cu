@@ -1527,14 +1527,23 @@ static unsigned grid_for(int64_t work_items, int64_t per_block, int waves_cap) {
 // Measured on B200 (C3/C4 short rows, C2 long rows): rows of <= 8 vectors
 // take pow2ceil(units) lanes (adjacent rows stay contiguous), up to 32
 // vectors 8 lanes, up to 64 vectors 16, longer rows the full warp.
-static int pick_row_group(int64_t nunits) {
+static int pick_row_group(int64_t nunits, int sb, bool peel) {
   if (nunits <= 8) {
     int G = 1;
     while (G < nunits) G <<= 1;
     return G;
   }
   if (nunits <= 32) return 8;
-  if (nunits <= 64) return 16;
+  if (peel) return nunits <= 64 ? 16 : 32;
+  // aligned rows, measured per row length on >= 1 GB views
+  // (profiles/r02_rows_ab/rowg_len.txt): 64 vectors -> 32 lanes (fp64 5.55
+  // -> 6.4, bf16 6.06 -> 6.5 TB/s, fp32 equal); 128 -> 8 lanes for 4- and
+  // 8-byte storage (16 vectors per lane: the double-buffered long-row loop;
+  // fp64 5.86 -> 6.69, fp32 6.02 -> 6.72; bf16 equal, kept at 32); 129-256 ->
+  // 16 (fp64 6.29 -> 6.71, fp32 6.37 -> 6.75, bf16 5.70 -> 6.13); longer: 32
+  if (nunits <= 64) return 32;
+  if (nunits <= 128) return sb >= 4 ? 8 : 32;
+  if (nunits <= 256) return 16;
   return 32;
 }
 
@@ -1777,7 +1786,7 @@ static void launch_rows_auto(const void* A, const void* x, void* y, int64_t u, i
                              int64_t su, C al, C be, int hb, cudaStream_t st) {
   constexpr int VEC = VecN<SD>::N;
   const int64_t nunits = std::max<int64_t>(1, nk / VEC);
-  int G = pick_row_group(nunits);
+  int G = pick_row_group(nunits, (int)sizeof(typename St<SD>::T), PEEL);
   static const int g_env = [] {  // TENVEC_B200_ROW_G: lanes per row, for A/B runs
     const char* e = getenv("TENVEC_B200_ROW_G");
     return e ? atoi(e) : 0;
