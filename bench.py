@@ -373,7 +373,7 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
             return sweep_graph.replay()
         return tv.dtvc_sweep(dt, xs)
 
-    clocks = ClockSampler() if rank == 0 else None
+    clocks = ClockSampler() if rank == 0 and not os.environ.get("TENVEC_BENCH_NO_CLOCKS") else None
     if clocks:
         clocks.start()
     for _ in range(args.warmup):
@@ -391,7 +391,7 @@ def run_sweep(args, tv, wl, world, rank) -> dict | None:
     # enqueues all K steps: a host stall during the loop (an nvidia-smi query
     # holding the driver lock cost one step 180 ms, profiles/r02_bench_variance/)
     # then cannot leave the GPU idle inside a timed step
-    _block_stream(torch, HOLD_CYCLES)
+    _hold(torch, world)
     for i in range(args.steps):
         if flush is not None:
             flush()
@@ -564,6 +564,18 @@ def _block_stream(torch, cycles: int = 2_000_000) -> None:
         torch.cuda._sleep(cycles)
 
 
+def _hold(torch, world: int) -> None:
+    """Hold the stream (HOLD_CYCLES) while the host enqueues a timed loop;
+    at N > 1 the ranks' streams then meet in a one-word NCCL all-reduce so the
+    first timed step does not absorb the skew between the ranks' holds (it
+    did: +1.5 ms on the first of 20 C2 steps at N = 4)."""
+    _block_stream(torch, HOLD_CYCLES)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(torch.zeros(1, device="cuda"))
+
+
 class L2Flush:
     """Evict the tensor from the 126 MB L2 between timed steps, untimed: write
     512 MB (the classic flush), then stream-read another 512 MB so the flush's
@@ -644,7 +656,7 @@ def run_with_assembly(args, tv, dt, xs, s, world, job_bytes_step) -> dict:
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n = max(3, min(args.steps, 10))
-        _block_stream(torch, HOLD_CYCLES)
+        _hold(torch, world)
         e0.record()
         for _ in range(n):
             astep()
@@ -795,7 +807,7 @@ def run_hopm(args, tv, wl, world, rank, key: str = "c4") -> dict | None:
     dt = tv.distribute_generated(shape, s, world, mode, fill="hash", seed=1, group=group)
     x0 = tv.initial_vectors(shape, mode)
     sweeps = args.steps
-    clocks = ClockSampler() if rank == 0 else None
+    clocks = ClockSampler() if rank == 0 and not os.environ.get("TENVEC_BENCH_NO_CLOCKS") else None
     if clocks:
         clocks.start()
     tv.dhopm3(dt, x0, sweeps=max(3, args.warmup))
@@ -807,7 +819,7 @@ def run_hopm(args, tv, wl, world, rank, key: str = "c4") -> dict | None:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     lib = tv._lib.load()
     n_launch0 = lib.tv_launch_count()
-    _block_stream(torch, HOLD_CYCLES)  # the host enqueues ahead (see run_sweep)
+    _hold(torch, world)  # the host enqueues ahead (see run_sweep)
     e0.record()
     res = tv.dhopm3(dt, x0, sweeps=sweeps)
     e1.record()

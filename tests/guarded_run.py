@@ -272,6 +272,56 @@ class Runner:
             self.bad.append(("vector_ops", n, name))
         print(("ok  " if ok else "BAD ") + str(("vector_ops", n, name, p)), flush=True)
 
+    def repack(self, u, ns, v, q, p, eb):
+        """tv_repack and tv_repack_part (the interleave assembly kernels) on
+        guarded parts and destinations vs plain buffers vs numpy."""
+        print("case repack", u, ns, v, q, p, eb, flush=True)
+        rng = np.random.default_rng(u * 7 + ns + p)
+        exts = [max(0, min(q, ns - r * q)) for r in range(p)]
+        parts = [rng.integers(0, 256, u * e * v * eb, dtype=np.uint8) for e in exts]
+        want = np.concatenate([pt.reshape(u, e * v * eb) for pt, e in zip(parts, exts)], axis=1).reshape(-1)
+        lib, sp = self.lib, _lib.stream_ptr()
+        results = {}
+        for where in ("guarded", "plain"):
+            keep = []
+
+            def buf(arr=None, nbytes=None):
+                if where == "guarded":
+                    return self.g(arr, nbytes).ptr
+                t = torch.empty(max(arr.nbytes if arr is not None else nbytes, 1), dtype=torch.uint8, device="cuda")
+                if arr is not None:
+                    t.copy_(torch.from_numpy(arr))
+                keep.append(t)
+                return t.data_ptr()
+
+            def read(ptr, count):
+                out = np.empty(count, dtype=np.uint8)
+                torch.cuda.synchronize()
+                _ok(drv.cuMemcpyDtoH(out.ctypes.data, ptr, out.nbytes))
+                return out
+
+            sptrs = [buf(pt) for pt in parts]
+            arr = (ctypes.c_void_p * p)(*sptrs)
+            dst = buf(nbytes=want.nbytes)
+            _lib.check(lib.tv_repack(arr, p, u, ns, v, q, eb, dst, sp), "repack")
+            got = read(dst, want.nbytes)
+            dst2 = buf(nbytes=want.nbytes)
+            for r in range(p):
+                if exts[r]:
+                    _lib.check(lib.tv_repack_part(sptrs[r], r, p, u, ns, v, q, eb, dst2, sp), "repack_part")
+            got2 = read(dst2, want.nbytes)
+            results[where] = (got, got2)
+            if where == "guarded":
+                torch.cuda.synchronize()
+                for b in self.bufs:
+                    b.free()
+                self.bufs.clear()
+        ok = all(np.array_equal(results[w][i], want) for w in results for i in (0, 1))
+        self.cases += 1
+        if not ok:
+            self.bad.append(("repack", u, ns, v, q, p, eb))
+        print(("ok  " if ok else "BAD ") + str(("repack", u, ns, v, q, p, eb)), flush=True)
+
     def tvc_normalize(self, shape, name):
         print("case tvc_normalize", shape, name, flush=True)
         mode = tv.MODES[name]
@@ -349,6 +399,11 @@ def main() -> int:
     for shape in [(3, 50, 7), (1, 4096, 1), (64, 33, 5)]:
         for name in ("f64", "bf16f32"):
             r.tvc_normalize(shape, name)
+    # interleave assembly: 16-byte short runs (thread per unit), unaligned and
+    # long runs (warp segments), a short last part
+    for u, ns, v, q, p, eb in [(1000, 6, 4, 3, 2, 4), (37, 10, 3, 4, 3, 2), (5, 4096, 1, 1024, 4, 8),
+                               (200, 96, 1, 48, 2, 4), (3, 7, 5, 3, 3, 8), (64, 96, 1, 24, 4, 4)]:
+        r.repack(u, ns, v, q, p, eb)
     print(f"DONE {r.cases} cases, {len(r.bad)} mismatches: {r.bad}", flush=True)
     return 1 if r.bad else 0
 
