@@ -2064,7 +2064,11 @@ static int launch_staged_tall(const void* A, const void* x, void* y, int64_t u, 
   const int maxv = v <= 4 ? 4 : v <= 8 ? 8 : v <= 12 ? 12 : v <= 16 ? 16 : v <= 24 ? 24 : 32;
   const size_t stride_b = (size_t)sbytes + 32 + ((size_t)maxv * sizeof(T) + 15) / 16 * 16;
   const size_t smem = 2 * stride_b + ((size_t)kWarps * maxv * sizeof(C) + 7) / 8 * 8 + 2 * sizeof(uint64_t);
-  const unsigned grid = (unsigned)std::min<int64_t>(u * nch, 2LL * sm_count());
+  // co-resident CTAs per SM: registers (__launch_bounds__(256, 2): up to 128
+  // per thread) allow 2, shared memory 2 at the default 48 KB stages (a third
+  // CTA per SM with 32 KB stages ran as a second wave: 3.75 -> 3.07 TB/s)
+  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(2, (int64_t)(227 * 1024) / (int64_t)(smem + 1024)));
+  const unsigned grid = (unsigned)std::min<int64_t>(u * nch, per_sm * sm_count());
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_k(kern, grid, kThreads, smem, st, (const T*)A, (const T*)x, (T*)y, u, nk, (int)v, nch, rpc, tr,

@@ -1,7 +1,7 @@
 #!/bin/bash
 # STAGED_TALL tile size A/B (TENVEC_B200_STAGE_BYTES)
 mkdir -p gpurun_out/tall
-for sb in 49152 32768 16384 8192; do
+for sb in 49152 32768 24576; do
   TENVEC_B200_STAGE_BYTES=$sb timeout 300 python scripts/tall_probe.py > gpurun_out/tall/stage_$sb.jsonl 2>&1
   echo "== stage=$sb"; python -c "
 import json
