@@ -1235,8 +1235,11 @@ __global__ void __launch_bounds__(kThreads)
 // then the 8 warps in order -- into the chunk's partial sums.
 constexpr int kTallRowsPerThread = 16;  // rows per tile <= 16 * kThreads
 
+#ifndef TV_TALL_OCC
+#define TV_TALL_OCC 2
+#endif
 template <int SD, typename C, int MAXV>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, TV_TALL_OCC)
     k_staged_tall(const typename St<SD>::T* __restrict__ A, const typename St<SD>::T* __restrict__ x,
                   typename St<SD>::T* __restrict__ y, int64_t u, int64_t nk, int v, int64_t nch, int64_t rpc,
                   int tr, int sbytes, C alpha, C beta, int has_beta, C* __restrict__ ws) {
@@ -2067,7 +2070,7 @@ static int launch_staged_tall(const void* A, const void* x, void* y, int64_t u, 
   // co-resident CTAs per SM: registers (__launch_bounds__(256, 2): up to 128
   // per thread) allow 2, shared memory 2 at the default 48 KB stages (a third
   // CTA per SM with 32 KB stages ran as a second wave: 3.75 -> 3.07 TB/s)
-  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(2, (int64_t)(227 * 1024) / (int64_t)(smem + 1024)));
+  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(TV_TALL_OCC, (int64_t)(227 * 1024) / (int64_t)(smem + 1024)));
   const unsigned grid = (unsigned)std::min<int64_t>(u * nch, per_sm * sm_count());
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
