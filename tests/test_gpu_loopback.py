@@ -10,6 +10,7 @@ WorkerGroup (comm.py:206-235): absent ranks named by a device barrier or a
 host collective that times out, kind mismatches, and the collective
 peer-memory fallback."""
 
+import os
 import warnings
 
 import numpy as np
@@ -22,13 +23,17 @@ from paper_2501_03121_b200._lib import to_host
 pytestmark = pytest.mark.gpu
 
 
-# world 8 is not run: 8 thread-ranks x their streams exceed the GPU's 32
-# hardware queues (CUDA_DEVICE_MAX_CONNECTIONS), two ranks' streams alias one
-# queue and a spinning barrier blocks the other rank's arrival (measured: the
-# host all_gather timed out); one process per GPU has no such aliasing
-@pytest.mark.parametrize("world", [2, 3, 4])
-def test_loopback_transports_match_oracle(tv, oracle, world):
+# world 8 runs with one owner-launch lane per rank: 8 thread-ranks with two
+# lanes each exceed the GPU's 32 hardware queues (CUDA_DEVICE_MAX_CONNECTIONS),
+# two ranks' streams then alias one queue and a spinning barrier blocks the
+# other rank's arrival (measured: the host all_gather timed out); one process
+# per GPU has no such aliasing
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_loopback_transports_match_oracle(tv, oracle, world, monkeypatch):
     from paper_2501_03121_b200.loopback import LoopbackWorld
+
+    if world > 4:
+        monkeypatch.setenv("TENVEC_B200_OWNER_LANES", "1")
 
     lw = LoopbackWorld(world, timeout=120)
     out = lw.run(lambda rank, tr: multirank_checks.run_checks(
