@@ -856,8 +856,11 @@ class RankGroup:
         """The "interleave" assembly across processes: every rank PUSHES its
         part's runs straight into every rank's joint copy in peer memory
         (tv_repack_part; NVLink stores are posted, loads would pay a round
-        trip each), then copies its own joint copy out; no NCCL.  False
-        (nothing done) when peer memory is not in use."""
+        trip each) -- from _MULTICAST_MIN ranks on, once, through the
+        buffer's NVSwitch multicast address (tv_repack_part_multicast) -- then
+        copies its own joint copy out; no NCCL.  Each rank picks its own way
+        (alignment, an empty part); the parts land in the same places either
+        way.  False (nothing done) when peer memory is not in use."""
         if self.size == 1 or self.algo not in ("fused", "p2p") or not local.is_cuda:
             return False
         p = self.size
