@@ -250,6 +250,13 @@ int tv_repack_part(const void* src, int r, int p, int64_t u, int64_t ns, int64_t
 int tv_repack_part_multicast(const void* src, int r, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
                              int elem_bytes, void* dst_mc, void* stream);
 
+/* tv_repack_part into ndst joint copies in ONE launch (this rank's and the
+ * peers', dsts = a HOST array of device pointers as mapped here): each
+ * 16-byte unit is read once and stored to every destination.  Needs 16-byte
+ * aligned buffers and runs (TV_EKERNEL else). */
+int tv_repack_part_peers(const void* src, int r, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
+                         int elem_bytes, void* const* dsts, int ndst, void* stream);
+
 /* Bytes at the start of a peer buffer reserved for the barrier words
  * (uint32 per rank); the transports put their data after it. */
 #define TV_PEER_HEADER 4096

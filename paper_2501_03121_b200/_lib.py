@@ -75,6 +75,8 @@ SIGNATURES = {
     "tv_dhopm3_plan_destroy": (_int, [_vp]),
     "tv_repack_part": (_int, [_vp, _int, _int, _i64, _i64, _i64, _i64, _int, _vp, _vp]),
     "tv_repack_part_multicast": (_int, [_vp, _int, _int, _i64, _i64, _i64, _i64, _int, _vp, _vp]),
+    "tv_repack_part_peers": (_int, [_vp, _int, _int, _i64, _i64, _i64, _i64, _int, ctypes.POINTER(_vp), _int,
+                                    _vp]),
     "tv_repack": (_int, [ctypes.POINTER(_vp), _int, _i64, _i64, _i64, _i64, _int, _vp, _vp]),
     "tv_peer_barrier": (_int, [ctypes.POINTER(_vp), _int, _int, ctypes.c_uint32, _i64, _vp, _vp]),
     "tv_preload": (_int, [ctypes.POINTER(_int)]),

@@ -350,6 +350,9 @@ def _env_int(name: str, default: int, lo: int) -> int:
 # buffer has one and the group has at least this many ranks
 # (TENVEC_B200_MULTICAST=0: always push to each peer)
 _MULTICAST_MIN = _env_int("TENVEC_B200_MULTICAST", 3, 0)
+# the per-peer push as one launch storing into every joint copy (A/B knob:
+# TENVEC_B200_PUSH_ONE_LAUNCH=0 launches one repack per destination)
+_PUSH_ONE_LAUNCH = os.environ.get("TENVEC_B200_PUSH_ONE_LAUNCH", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -891,6 +894,14 @@ class RankGroup:
             _lib.check(lib.tv_repack_part_multicast(local.data_ptr(), self.rank, p, u, plan.extent, v,
                                                     plan.chunk, eb, mc, stream), "interleave assembly")
             self.assembly_path = "multicast"
+        elif ext > 0 and _PUSH_ONE_LAUNCH and (local.data_ptr() | plan.chunk * v * eb | ext * v * eb
+                                               | plan.extent * v * eb) % 16 == 0 \
+                and all(pb.data(c) % 16 == 0 for c in range(p)):
+            # one launch stores every unit into all p joint copies
+            dsts = (ctypes.c_void_p * p)(*[pb.data((self.rank + j) % p) for j in range(p)])
+            _lib.check(lib.tv_repack_part_peers(local.data_ptr(), self.rank, p, u, plan.extent, v, plan.chunk, eb,
+                                                dsts, p, stream), "interleave assembly")
+            self.assembly_path = "push"
         else:
             self.assembly_path = "push"
             for j in range(p):  # own copy first, then the peers in ring order

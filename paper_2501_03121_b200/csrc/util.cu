@@ -410,6 +410,27 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The push of the interleave assembly to every joint copy in ONE kernel:
+// each 16-byte unit of part `only` is read once and stored into all ndst
+// destinations (this rank's joint copy and the peers', in peer memory), so
+// the stores to the different peers are in flight together instead of one
+// peer per launch (C3's 340 MB output at N = 4: 1.03 ms as three launches).
+struct Dsts {
+  char* p[TV_MAX_RANKS];
+};
+
+__global__ void __launch_bounds__(256)
+    k_repack_units_peers(const uint4* __restrict__ src, uint64_t total, uint64_t upr, uint64_t ext, uint64_t base,
+                         Dsts d, int ndst) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const uint64_t i = t / ext;
+    const uint64_t off = (i * upr + base + (t - i * ext)) * 16;
+    const uint4 w = ld_stream16(src + t);
+    for (int c = 0; c < ndst; ++c) *reinterpret_cast<uint4*>(d.p[c] + off) = w;
+  }
+}
+
 // ---------------------------------------------------------------- fill ----
 __host__ __device__ inline uint64_t fill_hash(uint64_t seed, uint64_t g) {
   uint64_t z = (g + 1ULL) * 0x9E3779B97F4A7C15ULL + seed * 0xD1B54A32D192ED03ULL;
@@ -711,6 +732,36 @@ extern "C" int tv_repack_part_multicast(const void* src, int r, int p, int64_t u
       static_cast<const uint4*>(src), (uint64_t)units, (uint64_t)(rowb / 16), (uint64_t)(extb / 16),
       (uint64_t)(r * qb / 16), static_cast<char*>(dst_mc));
   return launched("tv_repack_part_multicast");
+}
+
+extern "C" int tv_repack_part_peers(const void* src, int r, int p, int64_t u, int64_t ns, int64_t v, int64_t q,
+                                    int elem_bytes, void* const* dsts, int ndst, void* stream) {
+  using namespace tv;
+  if (r < 0 || r >= p || p > TV_MAX_RANKS || u < 0 || ns < 0 || v < 0 || q < 1 || (int64_t)r * q >= ns ||
+      ndst < 1 || ndst > TV_MAX_RANKS || !dsts ||
+      !(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8))
+    return set_error(TV_EKERNEL, "tv_repack_part_peers: bad arguments");
+  if (u == 0 || v == 0) return TV_OK;
+  const int64_t extb = std::min(q, ns - (int64_t)r * q) * v * elem_bytes;
+  const int64_t qb = q * v * elem_bytes, rowb = ns * v * elem_bytes;
+  uintptr_t al = reinterpret_cast<uintptr_t>(src) | (uintptr_t)extb | (uintptr_t)qb | (uintptr_t)rowb;
+  Dsts d{};
+  for (int c = 0; c < ndst; ++c) {
+    if (!dsts[c]) return set_error(TV_EKERNEL, "tv_repack_part_peers: null destination");
+    d.p[c] = static_cast<char*>(dsts[c]);
+    al |= reinterpret_cast<uintptr_t>(dsts[c]);
+  }
+  if (!src || (al & 15))
+    return set_error(TV_EKERNEL, "tv_repack_part_peers: needs 16-byte aligned runs and buffers");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t units = u * extb / 16;
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((units + 255) / 256, (int64_t)sms * 8));
+  k_repack_units_peers<<<g, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(src), (uint64_t)units, (uint64_t)(rowb / 16), (uint64_t)(extb / 16),
+      (uint64_t)(r * qb / 16), d, ndst);
+  return launched("tv_repack_part_peers");
 }
 
 static int repack_impl(const void* const* srcs, int p, int only, int64_t u, int64_t ns, int64_t v, int64_t q,
