@@ -310,13 +310,26 @@ class Runner:
                 if exts[r]:
                     _lib.check(lib.tv_repack_part(sptrs[r], r, p, u, ns, v, q, eb, dst2, sp), "repack_part")
             got2 = read(dst2, want.nbytes)
-            results[where] = (got, got2)
+            # the one-launch push into several joint copies (16-byte units only)
+            d3, d4 = buf(nbytes=want.nbytes), buf(nbytes=want.nbytes)
+            rb, qb = ns * v * eb, q * v * eb
+            for r in range(p):
+                eb_r = exts[r] * v * eb
+                if exts[r] and (sptrs[r] | d3 | d4 | rb | qb | eb_r) % 16 == 0:
+                    dsts = (ctypes.c_void_p * 2)(d3, d4)
+                    _lib.check(lib.tv_repack_part_peers(sptrs[r], r, p, u, ns, v, q, eb, dsts, 2, sp), "peers")
+                else:
+                    for dd in (d3, d4):
+                        if exts[r]:
+                            _lib.check(lib.tv_repack_part(sptrs[r], r, p, u, ns, v, q, eb, dd, sp), "part")
+            got3, got4 = read(d3, want.nbytes), read(d4, want.nbytes)
+            results[where] = (got, got2, got3, got4)
             if where == "guarded":
                 torch.cuda.synchronize()
                 for b in self.bufs:
                     b.free()
                 self.bufs.clear()
-        ok = all(np.array_equal(results[w][i], want) for w in results for i in (0, 1))
+        ok = all(np.array_equal(results[w][i], want) for w in results for i in range(4))
         self.cases += 1
         if not ok:
             self.bad.append(("repack", u, ns, v, q, p, eb))
